@@ -1,0 +1,278 @@
+// Batched blocked Gauss-Jordan inversion with partial pivoting (FP64).
+//
+// Replaces the reference's LU + gecon + lu_solve(I) / lu_solve(rhs) chain
+// (pkg/src/specdtn/leaf.py:104-121,152-161 and solver.py:108-136): the leading n x n block
+// of each M_i = [A | R] (n x ncols) is inverted in place and the trailing columns become
+// inv(A) R. The pivot sequence is that of LAPACK dgetrf (the candidate rows of column j
+// in GJ are exactly the rows of LU's Schur complement; ties keep the smallest row index).
+//
+// Per column block J = [k0, k0+kb):
+//   1. gj_panel    : one CTA per matrix factors the n x kb panel in shared memory (warp
+//                    argmax pivot search, row swap, scale, eliminate all other rows) giving
+//                    panel = [inv(B_JJ) ; -B_RJ inv(B_JJ)] (rows J after swaps).
+//   2. gj_swapcopy : applies the kb row interchanges to every other column and saves the
+//                    kb pivot rows W = B_J,C (they are overwritten by step 3).
+//   3. DMMA update (gemm_dmma.cu MODE_GJ_UPD): B_J,C = panel_J W,  B_R,C += panel_R W.
+// Finally the column interchanges are undone: inv(A)[:, perm[j]] = M[:, j].
+//
+// Work: 2 n^2 ncols flops (= (2/3)n^3 LU + (4/3)n^3 inverse + 2 n^2 (ncols-n) for the RHS),
+// all but the 2 n kb^2 per panel on DMMA tiles.
+#include "hps_common.cuh"
+#include "hps_kernels.cuh"
+
+namespace hps {
+
+constexpr int GJ_THREADS = 256;
+constexpr int GJ_SMEM_BUDGET = 220 * 1024;
+
+static int gj_panel_width(int n) {
+  int kb = GJ_SMEM_BUDGET / (8 * n) - 2;  // n*(kb+1) doubles of panel + pivot row + scratch
+  if (kb > 32) kb = 32;
+  if (kb > n) kb = n;
+  if (kb > 4) kb &= ~3;
+  return kb < 1 ? 1 : kb;
+}
+
+// W (batch x kb x ncols doubles) followed by the inverse column permutation (batch x n ints)
+long long gj_workspace_doubles(int batch, int n, int ncols) {
+  return (long long)batch * gj_panel_width(n) * ncols + ((long long)batch * n + 1) / 2 + 1;
+}
+
+__global__ void __launch_bounds__(GJ_THREADS) gj_panel_kernel(int n, int k0, int kb, MatB M, int* piv,
+                                                              int* status, int batch_off) {
+  extern __shared__ double sm[];
+  const int ldp = kb + 1;  // odd stride: row-per-thread access is bank-conflict free
+  double* P = sm;
+  double* prow = P + (size_t)n * ldp;
+  double* rv = prow + 32;
+  int* ri = reinterpret_cast<int*>(rv + 8);
+
+  const int item = blockIdx.x + batch_off;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* Mi = M.get(item);
+  const long long ld = M.ld;
+
+  for (int e = tid; e < n * kb; e += GJ_THREADS) {
+    const int r = e / kb, c = e - r * kb;
+    P[r * ldp + c] = Mi[r * ld + k0 + c];
+  }
+  __syncthreads();
+
+  for (int j = 0; j < kb; ++j) {
+    const int cj = k0 + j;
+    double best = -1.0;
+    int bi = n;
+    for (int i = cj + tid; i < n; i += GJ_THREADS) {
+      const double v = fabs(P[i * ldp + j]);
+      if (v > best) { best = v; bi = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if (lane == 0) { rv[warp] = best; ri[warp] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      double b = rv[0];
+      int bix = ri[0];
+      for (int w = 1; w < GJ_THREADS / 32; ++w)
+        if (rv[w] > b || (rv[w] == b && ri[w] < bix)) { b = rv[w]; bix = ri[w]; }
+      if (bix >= n) bix = cj;  // all candidates NaN: keep the diagonal, NaN propagates
+      if (!(b > 0.0) && status) status[item] |= 1;
+      ri[8] = bix;
+      piv[(long long)item * n + cj] = bix;
+    }
+    __syncthreads();
+    const int pr = ri[8];
+    if (pr != cj && tid < kb) {
+      const double t = P[pr * ldp + tid];
+      P[pr * ldp + tid] = P[cj * ldp + tid];
+      P[cj * ldp + tid] = t;
+    }
+    __syncthreads();
+    if (tid < kb) {
+      const double inv = 1.0 / P[cj * ldp + j];
+      prow[tid] = (tid == j) ? inv : P[cj * ldp + tid] * inv;
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += GJ_THREADS) {
+      double* row = P + i * ldp;
+      if (i == cj) {
+        for (int jj = 0; jj < kb; ++jj) row[jj] = prow[jj];
+      } else {
+        const double f = row[j];
+        row[j] = 0.0;
+        for (int jj = 0; jj < kb; ++jj) row[jj] -= f * prow[jj];
+      }
+    }
+    __syncthreads();
+  }
+
+  for (int e = tid; e < n * kb; e += GJ_THREADS) {
+    const int r = e / kb, c = e - r * kb;
+    Mi[r * ld + k0 + c] = P[r * ldp + c];
+  }
+}
+
+// one thread per non-panel column: apply the panel's row swaps, save the pivot rows to W
+__global__ void gj_swapcopy_kernel(int n, int ncols, int k0, int kb, MatB M, const int* piv, MatB W,
+                                   int batch_off) {
+  const int item = blockIdx.y + batch_off;
+  const int cl = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cl >= ncols - kb) return;
+  const int c = cl < k0 ? cl : cl + kb;
+  double* Mi = M.get(item);
+  const long long ld = M.ld;
+  const int* pv = piv + (long long)item * n + k0;
+  for (int j = 0; j < kb; ++j) {
+    const int r = pv[j];
+    if (r != k0 + j) {
+      const double t = Mi[(long long)r * ld + c];
+      Mi[(long long)r * ld + c] = Mi[(long long)(k0 + j) * ld + c];
+      Mi[(long long)(k0 + j) * ld + c] = t;
+    }
+  }
+  double* Wi = W.get(item);
+  for (int j = 0; j < kb; ++j) Wi[(long long)j * W.ld + c] = Mi[(long long)(k0 + j) * ld + c];
+}
+
+// inverse column permutation pinv (pinv[perm[j]] = j) from the LAPACK interchange list
+__global__ void gj_perm_kernel(int n, const int* piv, int* pinv, int batch_off) {
+  extern __shared__ int perm[];
+  const int item = blockIdx.x + batch_off;
+  const int* pv = piv + (long long)item * n;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) perm[j] = j;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < n; ++j) {
+      const int r = pv[j];
+      const int t = perm[j];
+      perm[j] = perm[r];
+      perm[r] = t;
+    }
+  }
+  __syncthreads();
+  int* out = pinv + (long long)item * n;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) out[perm[j]] = j;
+}
+
+// F[r][c] = M[r][pinv[c]] for c < n, one warp per row, row staged in shared memory
+__global__ void gj_unpermute_kernel(int n, MatB M, const int* pinv, int rows_per_cta, int batch_off) {
+  extern __shared__ double rowbuf[];
+  const int item = blockIdx.y + batch_off;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  double* buf = rowbuf + (size_t)warp * n;
+  double* Mi = M.get(item);
+  const int* pi = pinv + (long long)item * n;
+  const int r0 = blockIdx.x * rows_per_cta;
+  const int r1 = min(n, r0 + rows_per_cta);
+  for (int r = r0 + warp; r < r1; r += nw) {
+    double* row = Mi + (long long)r * M.ld;
+    for (int c = lane; c < n; c += 32) buf[c] = row[c];
+    __syncwarp();
+    for (int c = lane; c < n; c += 32) row[c] = buf[pi[c]];
+    __syncwarp();
+  }
+}
+
+// out[item] = max_c sum_r |M[r][c]| over the leading n x n block (atomic max on the bit
+// pattern: valid for non-negative doubles and lets NaN win)
+__global__ void colnorm1_kernel(int n, MatB M, unsigned long long* out, int batch_off) {
+  const int item = blockIdx.y + batch_off;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  double s = 0.0;
+  if (c < n) {
+    const double* Mi = M.get(item);
+    for (int r = 0; r < n; ++r) s += fabs(Mi[(long long)r * M.ld + c]);
+  }
+  __shared__ double red[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double t = __shfl_xor_sync(0xffffffffu, s, o);
+    s = (t > s || t != t) ? t : s;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = (red[w] > m || red[w] != red[w]) ? red[w] : m;
+    atomicMax(out + item, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+int launch_colnorm1(int batch, int n, MatB M, double* out, cudaStream_t s) {
+  cudaMemsetAsync(out, 0, sizeof(double) * batch, s);
+  for (int off = 0; off < batch; off += 65535) {
+    const int nb = min(65535, batch - off);
+    dim3 grid((n + 255) / 256, nb);
+    colnorm1_kernel<<<grid, 256, 0, s>>>(n, M, reinterpret_cast<unsigned long long*>(out), off);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
+int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, double* anorm,
+              double* ainvnorm, int* status, cudaStream_t s) {
+  if (batch <= 0 || n <= 0) return 0;
+  if (anorm) {
+    int rc = launch_colnorm1(batch, n, M, anorm, s);
+    if (rc) return rc;
+  }
+  const int kbmax = gj_panel_width(n);
+  const size_t psmem = sizeof(double) * ((size_t)n * (kbmax + 1) + 32 + 8) + sizeof(int) * 16;
+  static int configured_smem = 0;
+  if ((int)psmem > 48 * 1024 && (int)psmem > configured_smem) {
+    cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+    configured_smem = (int)psmem;
+  }
+  MatB W{wbuf, (long long)kbmax * ncols, nullptr, ncols, 0};
+  for (int k0 = 0; k0 < n; k0 += kbmax) {
+    const int kb = min(kbmax, n - k0);
+    const size_t smem = sizeof(double) * ((size_t)n * (kb + 1) + 32 + 8) + sizeof(int) * 16;
+    for (int off = 0; off < batch; off += 65535) {
+      const int nb = min(65535, batch - off);
+      gj_panel_kernel<<<nb, GJ_THREADS, smem, s>>>(n, k0, kb, M, piv, status, off);
+      if (ncols > kb) {
+        dim3 g2((ncols - kb + 127) / 128, nb);
+        gj_swapcopy_kernel<<<g2, 128, 0, s>>>(n, ncols, k0, kb, M, piv, W, off);
+      }
+    }
+    if (ncols > kb) {
+      GemmArgs g{};
+      g.M = n;
+      g.N = ncols - kb;
+      g.K = kb;
+      g.alpha = 1.0;
+      g.beta = 1.0;
+      g.A = M;
+      g.A.off = M.off + k0;
+      g.B = W;
+      g.C = M;
+      g.k0 = k0;
+      g.kb = kb;
+      int rc = launch_gemm(g, batch, MODE_GJ_UPD, s);
+      if (rc) return rc;
+    }
+  }
+  // undo the column interchanges of the inverse block (pinv lives in the workspace after W)
+  int* pinv = reinterpret_cast<int*>(wbuf + (size_t)batch * kbmax * ncols);
+  for (int off = 0; off < batch; off += 65535) {
+    const int nb = min(65535, batch - off);
+    gj_perm_kernel<<<nb, 128, sizeof(int) * n, s>>>(n, piv, pinv, off);
+    const int rows_per_cta = 32;
+    const size_t usmem = sizeof(double) * (size_t)n * 4;
+    if (usmem > 48 * 1024)
+      cudaFuncSetAttribute(gj_unpermute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem);
+    dim3 g3((n + rows_per_cta - 1) / rows_per_cta, nb);
+    gj_unpermute_kernel<<<g3, 128, usmem, s>>>(n, M, pinv, rows_per_cta, off);
+  }
+  if (ainvnorm) {
+    int rc = launch_colnorm1(batch, n, M, ainvnorm, s);
+    if (rc) return rc;
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
+}  // namespace hps

@@ -1,0 +1,198 @@
+// extern "C" entry points (include/hps_b200.h) -> internal launchers.
+#include "../../include/hps_b200.h"
+#include "hps_kernels.cuh"
+
+using namespace hps;
+
+static MatB to_matb(const hps_mat_batch* m) {
+  MatB r{};
+  r.base = m->base;
+  r.stride = m->stride;
+  r.ptrs = m->ptrs;
+  r.ld = m->ld;
+  r.off = m->off;
+  return r;
+}
+static MatB dense(double* base, long long stride, int ld, long long off = 0) {
+  MatB r{};
+  r.base = base;
+  r.stride = stride;
+  r.ld = ld;
+  r.off = off;
+  return r;
+}
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+extern "C" {
+
+int hps_abi_version(void) { return HPS_ABI_VERSION; }
+
+const char* hps_status_string(int code) {
+  switch (code) {
+    case HPS_OK: return "ok";
+    case HPS_EINVAL: return "invalid argument";
+    case HPS_ECUDA: return cudaGetErrorString(cudaGetLastError());
+    default: return "unknown status";
+  }
+}
+
+int hps_gemm_batched(int batch, int M, int N, int K, double alpha, const hps_mat_batch* A,
+                     const hps_mat_batch* B, double beta, const hps_mat_batch* C, const double* bias,
+                     int ldbias, void* stream) {
+  if (!A || !B || !C || batch < 0 || M < 0 || N < 0 || K < 0) return HPS_EINVAL;
+  GemmArgs g{};
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.alpha = alpha;
+  g.beta = beta;
+  g.A = to_matb(A);
+  g.B = to_matb(B);
+  g.C = to_matb(C);
+  g.bias = bias;
+  g.ldbias = ldbias;
+  return launch_gemm(g, batch, MODE_GEMM, (cudaStream_t)stream);
+}
+
+long long hps_gj_workspace_bytes(int batch, int n, int ncols) {
+  return 8 * gj_workspace_doubles(batch, n, ncols);
+}
+
+int hps_gj_invert_batched(int batch, int n, int ncols, const hps_mat_batch* M, int* piv, void* workspace,
+                          double* anorm, double* ainvnorm, int* status, void* stream) {
+  if (!M || !piv || !workspace || n <= 0 || ncols < n) return HPS_EINVAL;
+  return gj_invert(batch, n, ncols, to_matb(M), piv, (double*)workspace, anorm, ainvnorm, status,
+                   (cudaStream_t)stream);
+}
+
+long long hps_leaf_workspace_bytes(int nleaf, int p, int q) {
+  const long long m = (long long)(p - 2) * (p - 2), b = 4LL * q, c = 4LL * (p - 1);
+  return align256(8 * nleaf * m * c) + align256(4 * nleaf * m) + hps_gj_workspace_bytes(nleaf, (int)m, (int)(m + b));
+}
+
+int hps_leaf_build(const hps_leaf_batch* L, void* stream) {
+  if (!L || L->nleaf <= 0 || L->p < 3 || L->q < 2 || L->p < L->q + 1) return HPS_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int p = L->p, q = L->q, nl = L->nleaf;
+  const int m = (p - 2) * (p - 2), b = 4 * q, c = 4 * (p - 1);
+  char* ws = (char*)L->workspace;
+  double* aie = (double*)ws;
+  int* piv = (int*)(ws + align256(8ull * nl * m * c));
+  void* gjw = ws + align256(8ull * nl * m * c) + align256(4ull * nl * m);
+  const long long sfs = (long long)m * (m + b);
+
+  LeafAsmArgs a{};
+  a.nleaf = nl;
+  a.p = p;
+  a.coef = L->coef;
+  a.dx = L->dx;
+  a.dy = L->dy;
+  a.dxx = L->dxx;
+  a.dyy = L->dyy;
+  a.int_pos = L->int_pos;
+  a.ext_pos = L->ext_pos;
+  a.Aii = dense(L->fs, sfs, m + b);
+  a.Aie = dense(aie, (long long)m * c, c);
+  int rc = launch_leaf_assemble(a, s);
+  if (rc) return rc;
+
+  // right-hand sides of the interior solve: fs[:, m:] = -A_ie L   (leaf.py:154)
+  GemmArgs g{};
+  g.M = m;
+  g.N = b;
+  g.K = c;
+  g.alpha = -1.0;
+  g.beta = 0.0;
+  g.A = dense(aie, (long long)m * c, c);
+  g.B = dense(const_cast<double*>(L->lift), 0, b);
+  g.C = dense(L->fs, sfs, m + b, m);
+  if ((rc = launch_gemm(g, nl, MODE_GEMM, s))) return rc;
+
+  // [F | S] = inv(A_ii) [I | -A_ie L]
+  if ((rc = gj_invert(nl, m, m + b, dense(L->fs, sfs, m + b), piv, (double*)gjw, L->anorm, L->ainvnorm,
+                      L->status, s)))
+    return rc;
+
+  // H = D_fi F   (leaf.py:162; exterior rows of F are zero)
+  g = GemmArgs{};
+  g.M = b;
+  g.N = m;
+  g.K = m;
+  g.alpha = 1.0;
+  g.beta = 0.0;
+  g.A = dense(const_cast<double*>(L->dfi), 0, m);
+  g.B = dense(L->fs, sfs, m + b);
+  g.C = dense(L->h, (long long)b * m, m);
+  if ((rc = launch_gemm(g, nl, MODE_GEMM, s))) return rc;
+
+  // T = D_fi S_ie + D_fe L   (leaf.py:155; exterior rows of S are the lift)
+  g.N = b;
+  g.B = dense(L->fs, sfs, m + b, m);
+  g.C = dense(L->t, (long long)b * b, b);
+  g.bias = L->t0;
+  g.ldbias = b;
+  return launch_gemm(g, nl, MODE_GEMM, s);
+}
+
+long long hps_merge_workspace_bytes(int npar, int m3, int e) {
+  return align256(4ull * npar * m3) + hps_gj_workspace_bytes(npar, m3, m3 + e);
+}
+
+int hps_merge_build(const hps_merge_batch* Mb, void* stream) {
+  if (!Mb || Mb->npar <= 0 || Mb->m3 <= 0 || Mb->n1 < 0 || Mb->n2 < 0) return HPS_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int np = Mb->npar, m3 = Mb->m3, e = Mb->n1 + Mb->n2;
+  char* ws = (char*)Mb->workspace;
+  int* piv = (int*)ws;
+  void* gjw = ws + align256(4ull * np * m3);
+  const long long sxs = (long long)m3 * (m3 + e);
+
+  MergeGatherArgs a{};
+  a.npar = np;
+  a.m3 = m3;
+  a.n1 = Mb->n1;
+  a.n2 = Mb->n2;
+  a.Ta = MatB{nullptr, 0, Mb->ta, Mb->lda, 0};
+  a.Tb = MatB{nullptr, 0, Mb->tb, Mb->ldb, 0};
+  a.idx = Mb->idx;
+  a.idx_stride = Mb->idx_stride;
+  a.XS = dense(Mb->xs, sxs, m3 + e);
+  a.Tei = dense(Mb->tei, (long long)e * m3, m3);
+  a.Tnew = dense(Mb->tnew, (long long)e * e, e);
+  int rc = launch_merge_gather(a, s);
+  if (rc) return rc;
+
+  if ((rc = gj_invert(np, m3, m3 + e, dense(Mb->xs, sxs, m3 + e), piv, (double*)gjw, Mb->dnorm, Mb->xnorm,
+                      Mb->status, s)))
+    return rc;
+
+  // T_new = blkdiag + T_ei S   (solver.py:139-141)
+  GemmArgs g{};
+  g.M = e;
+  g.N = e;
+  g.K = m3;
+  g.alpha = 1.0;
+  g.beta = 1.0;
+  g.A = dense(Mb->tei, (long long)e * m3, m3);
+  g.B = dense(Mb->xs, sxs, m3 + e, m3);
+  g.C = dense(Mb->tnew, (long long)e * e, e);
+  return launch_gemm(g, np, MODE_GEMM, s);
+}
+
+int hps_sweep_gemv(const hps_gemv_batch* gb, void* stream) {
+  if (!gb || !gb->pool || !gb->xidx || !gb->oidx || gb->nrhs < 1 || gb->nrhs > 16) return HPS_EINVAL;
+  GemvArgs a{};
+  a.nitems = gb->nitems;
+  a.R = gb->R;
+  a.K = gb->K;
+  a.nrhs = gb->nrhs;
+  a.A = to_matb(&gb->A);
+  a.pool = gb->pool;
+  a.xidx = gb->xidx;
+  a.x2idx = gb->x2idx;
+  a.aidx = gb->aidx;
+  a.oidx = gb->oidx;
+  return launch_gemv_gather(a, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+// Internal launch interface shared by the kernel translation units and the C-ABI layer.
+#pragma once
+#include "hps_common.cuh"
+
+namespace hps {
+
+enum { MODE_GEMM = 0, MODE_GJ_UPD = 1 };
+
+struct GemmArgs {
+  int M, N, K;
+  double alpha, beta;
+  MatB A, B, C;
+  const double* bias;  // MODE_GEMM: optional M x N matrix shared by the batch, added in the epilogue
+  int ldbias;
+  int k0, kb;          // MODE_GJ_UPD only
+};
+
+int launch_gemm(const GemmArgs& g, int batch, int mode, cudaStream_t s);
+
+// Blocked Gauss-Jordan inversion with partial pivoting of the leading n x n block of each
+// M_i (n x ncols, row-major, ld); the trailing ncols-n columns are right-hand sides that end
+// up multiplied by the inverse. piv: batch x n (LAPACK-style row interchanges), wbuf:
+// workspace (see gj_workspace_doubles). On exit M_i[:, :n] = inv(A_i) (columns un-permuted),
+// M_i[:, n:] = inv(A_i) * rhs_i. anorm/ainvnorm (may be null): 1-norms before/after.
+long long gj_workspace_doubles(int batch, int n, int ncols);
+int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, double* anorm,
+              double* ainvnorm, int* status, cudaStream_t s);
+
+int launch_colnorm1(int batch, int n, MatB M, double* out, cudaStream_t s);
+
+// Leaf-stage assembly: interior rows of the collocation matrix for each leaf.
+struct LeafAsmArgs {
+  int nleaf, p;
+  const double* coef;      // [6][nleaf][p*p]
+  const double* dx;        // p x p 1D operators of this leaf shape
+  const double* dy;
+  const double* dxx;
+  const double* dyy;
+  const int* int_pos;      // [p*p] position in i_ci or -1
+  const int* ext_pos;      // [p*p] position in i_ce or -1
+  MatB Aii;                // m x (m+b) (only the first m columns written)
+  MatB Aie;                // m x c
+};
+int launch_leaf_assemble(const LeafAsmArgs& a, cudaStream_t s);
+
+// Merge gather: builds [Delta | -Ta31 | Tb32], Tei = [Ta13; Tb23], Tnew = blkdiag(Ta11, Tb22)
+struct MergeGatherArgs {
+  int npar, m3, n1, n2;
+  MatB Ta, Tb;              // child DtN maps (ld = child exterior size)
+  const int* idx;           // per parent: [p1a(n1) | p3a(m3) | p2b(n2) | p3b(m3)]
+  long long idx_stride;     // 0 when all parents share one index set
+  MatB XS;                  // m3 x (m3 + e)
+  MatB Tei;                 // e x m3
+  MatB Tnew;                // e x e
+};
+int launch_merge_gather(const MergeGatherArgs& a, cudaStream_t s);
+
+// Solve-stage batched gather-GEMV: for item i, rows r < R, rhs j < nrhs:
+//   y[oidx[i][r]][j] = sum_k A_i[r][k] * x_i[k][j] + (aidx ? pool[aidx[i][r]][j] : 0)
+//   x_i[k][j] = pool[xidx[i][k]][j] - (x2idx ? pool[x2idx[i][k]][j] : 0)
+// pool is a single (rows x nrhs) vector arena; every index is an absolute pool row.
+struct GemvArgs {
+  int nitems, R, K, nrhs;
+  MatB A;
+  double* pool;
+  const int* xidx;   // [nitems][K]
+  const int* x2idx;  // [nitems][K] or null
+  const int* aidx;   // [nitems][R] or null
+  const int* oidx;   // [nitems][R]
+};
+int launch_gemv_gather(const GemvArgs& a, cudaStream_t s);
+
+}  // namespace hps

@@ -1,0 +1,687 @@
+"""Drop-in ``build_stage`` / ``FactorizedSolver.solve`` running the HPS hot path on one B200.
+
+Mirrors the reference entry points (pkg/src/specdtn/solver.py):
+  build_stage(tree, spec, p, q, mode="stored", plan=None, order=None)   solver.py:357-415
+  FactorizedSolver.solve(f=None, g=None) -> SolveState                   solver.py:337-354
+  solve / upward_pass / downward_pass                                    solver.py:418-437
+with the same argument conventions, output layout and exception types/messages
+(LeafSingularError leaf.py:40-41,118-120; MergeSingularError solver.py:58-59,113-118).
+
+Execution is level-synchronous instead of node-by-node: all leaves of one shape go through
+one ``hps_leaf_build`` call, all parents of one depth and interface shape through one
+``hps_merge_build`` call, and each solve-sweep level is one ``hps_sweep_gemv`` call per
+shape group (C ABI in include/hps_b200.h). The reference's order-independence
+(test_solver.py:205-217) is what makes this legal; ``order`` is still validated.
+Operators stay resident in HBM as torch tensors owned by the solver object.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+import warnings
+from collections.abc import Mapping
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _ext
+from . import coeffs as coeff_mod
+from .geometry import enumerate_gauss_nodes
+from .spectral import edge_interpolators, shape_constants
+
+RCOND_FLOOR = 1e-13
+BUILD_COUNT = 0
+
+
+class LeafSingularError(RuntimeError):
+    """Interior collocation block is (numerically) singular on some leaf."""
+
+
+class MergeSingularError(RuntimeError):
+    """The interface operator difference is numerically singular."""
+
+
+def _device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1612_02736_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _stream_ptr():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _i32(a, dev):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=dev)
+
+
+def _f64(a, dev):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=dev)
+
+
+def _ptr_array(ptrs, dev):
+    return torch.as_tensor(np.asarray(ptrs, dtype=np.int64), device=dev)
+
+
+class LeafSolutions(Mapping):
+    """leaf id -> (P,) tabulation, backed by one host array (no per-leaf copies)."""
+
+    def __init__(self, ids, rows, table):
+        self._row = {int(n): int(r) for n, r in zip(ids, rows)}
+        self._table = table
+
+    def __getitem__(self, nid):
+        return self._table[self._row[int(nid)]]
+
+    def __iter__(self):
+        return iter(self._row)
+
+    def __len__(self):
+        return len(self._row)
+
+
+@dataclass
+class SolveState:
+    """Result of one solve (reference solver.py:191-210)."""
+
+    u: np.ndarray
+    w: np.ndarray | None = None
+    leaf_solutions: Mapping = field(default_factory=dict)
+    g_tab: Mapping = field(default_factory=dict)
+    h_root: np.ndarray | None = None
+    solve_seconds: float = 0.0
+    tree: object = None
+    p: int = 0
+    q: int = 0
+    scratch: dict | None = None
+
+
+@dataclass
+class _LeafGroup:
+    key: tuple
+    ids: list
+    sc: object
+    fs: torch.Tensor = None
+    h: torch.Tensor = None
+    anorm: torch.Tensor = None
+    ainvnorm: torch.Tensor = None
+    status: torch.Tensor = None
+    consts: dict = None
+    first_row: int = 0     # global leaf row of slot 0 (G / UC regions)
+
+
+@dataclass
+class _ParentGroup:
+    depth: int
+    ids: list
+    m3: int
+    n1: int
+    n2: int
+    lda: int
+    ldb: int
+    xs: torch.Tensor = None
+    tei: torch.Tensor = None
+    tnew: torch.Tensor = None
+    dnorm: torch.Tensor = None
+    xnorm: torch.Tensor = None
+    status: torch.Tensor = None
+    wrap: dict = None      # singleton wrapped parent: qd, qu, pu, pd, ec, xsw, tw
+
+    @property
+    def e(self):
+        return self.n1 + self.n2
+
+
+class FactorizedSolver:
+    """Built hierarchy of operators, resident on the GPU (reference solver.py:213-237)."""
+
+    def __init__(self, tree, plan, spec, p, q, mode):
+        self.tree, self.plan, self.spec = tree, plan, spec
+        self.p, self.q, self.mode = p, q, mode
+        self.build_seconds = 0.0
+        self.device = _device()
+        self.leaf_groups: list[_LeafGroup] = []
+        self.parent_groups: list[_ParentGroup] = []
+        self.leaf_loc: dict = {}       # leaf id -> (group index, slot)
+        self.depth: dict = {}
+        self._sweeps: dict = {}        # nrhs -> compiled sweep program
+        self.events: dict = {}
+
+    # -- accounting -------------------------------------------------------------------------
+    def leaf_memory_floats(self) -> int:
+        """Reference-equivalent retained leaf floats: S (P x b) + F (P x m) + H (b x m)."""
+        if self.mode == "econ":
+            return 0
+        p, q = self.p, self.q
+        P, m, b = p * p, (p - 2) ** 2, 4 * q
+        return sum(len(g.ids) for g in self.leaf_groups) * (P * b + P * m + b * m)
+
+    def memory_floats(self) -> int:
+        total = self.leaf_memory_floats()
+        for g in self.parent_groups:
+            if g.wrap is not None:
+                ec = g.wrap["ec"]
+                total += g.m3 * g.m3 + g.m3 * ec + g.e * g.m3 + g.wrap["pu"].size + g.wrap["pd"].size
+            else:
+                total += len(g.ids) * (g.m3 * g.m3 + g.m3 * g.e + g.e * g.m3)
+        return total
+
+    def device_bytes(self) -> int:
+        n = 0
+        for g in self.leaf_groups:
+            n += sum(t.numel() * t.element_size() for t in (g.fs, g.h) if t is not None)
+        for g in self.parent_groups:
+            if g.wrap is not None:
+                n += g.wrap["xsw"].numel() * 8 + g.tei.numel() * 8
+            else:
+                n += (g.xs.numel() + g.tei.numel()) * 8
+        return n
+
+    # -- solve stage ------------------------------------------------------------------------
+    def _leaf_table(self, g):
+        """(n_leaves, m) interior body-load table in leaf-row order (solver.py:241-253)."""
+        if g is None:
+            g = self.spec.body_load
+        nl = self._n_leaves
+        m = (self.p - 2) ** 2
+        if g is None:
+            return np.zeros((nl, m))
+        if isinstance(g, torch.Tensor) or isinstance(g, np.ndarray):
+            arr = g if isinstance(g, torch.Tensor) else np.asarray(g, dtype=float)
+            if tuple(arr.shape) != (nl, m):
+                raise ValueError(f"load table has shape {tuple(arr.shape)}, expected ({nl}, {m})")
+            return arr
+        out = np.empty((nl, m))
+        if callable(g):
+            for grp in self.leaf_groups:
+                pts = self._interior_points(grp)
+                vals = np.asarray(g(pts.reshape(-1, 2)), dtype=float).reshape(len(grp.ids), m)
+                out[grp.first_row:grp.first_row + len(grp.ids)] = vals
+            return out
+        for grp in self.leaf_groups:
+            for slot, nid in enumerate(grp.ids):
+                g_ci = np.asarray(g[nid], dtype=float)
+                if g_ci.shape != (m,):
+                    raise ValueError(f"leaf {nid} load has shape {g_ci.shape}, expected ({m},)")
+                out[grp.first_row + slot] = g_ci
+        return out
+
+    def _interior_points(self, grp):
+        sc = grp.sc
+        pts0 = sc.cheb2d()[sc.i_ci]
+        org = np.array([[self.tree.nodes[n].bounds.x1lo, self.tree.nodes[n].bounds.x2lo] for n in grp.ids])
+        return pts0[None, :, :] + org[:, None, :]
+
+    def _dirichlet(self, f):
+        root_ext = self.plan.node[self.tree.root].ext
+        if f is None:
+            f = self.spec.dirichlet
+        if f is None:
+            return np.zeros(root_ext.size)
+        if callable(f):
+            return np.asarray(f(self.plan.coords[root_ext]), dtype=float)
+        vals = f if isinstance(f, torch.Tensor) else np.asarray(f, dtype=float)
+        if tuple(vals.shape) != (root_ext.size,):
+            raise ValueError(f"boundary data has shape {tuple(vals.shape)}, expected ({root_ext.size},)")
+        return vals
+
+    def solve(self, f=None, g=None) -> SolveState:
+        """Two-pass solve for Dirichlet data f and body load g (reference solver.py:337-354)."""
+        t0 = time.perf_counter()
+        st = self._solve_host(f, g, down=True)
+        st.solve_seconds = time.perf_counter() - t0
+        return st
+
+    def _solve_host(self, f, g, down=True) -> SolveState:
+        fv = self._dirichlet(f) if down else None
+        gt = self._leaf_table(g)
+        prog = self._program(1)
+        lay, pool = self._layout, prog["pool"]
+        gdev = torch.as_tensor(gt, dtype=torch.float64).to(self.device, non_blocking=True).reshape(-1, 1)
+        fdev = None
+        if down:
+            fdev = torch.as_tensor(fv, dtype=torch.float64).to(self.device, non_blocking=True).reshape(-1, 1)
+        self._run(prog, fdev, gdev, down=down)
+        host = pool[:, 0].cpu().numpy()
+        N = self.plan.n_gauss
+        rs = lay["hslot"][self.tree.root]
+        st = SolveState(u=host[lay["U"]:lay["U"] + N].copy(), w=host[lay["W"]:lay["W"] + N].copy(),
+                        tree=self.tree, p=self.p, q=self.q,
+                        h_root=host[rs:rs + lay["hsize"][self.tree.root]].copy())
+        gtab = gt.detach().cpu().numpy() if isinstance(gt, torch.Tensor) else np.asarray(gt)
+        st.g_tab = LeafSolutions(self._leaf_ids, range(self._n_leaves), gtab)
+        if down:
+            P = self.p ** 2
+            uc = host[lay["UC"]:lay["UC"] + self._n_leaves * P].reshape(self._n_leaves, P).copy()
+            st.leaf_solutions = LeafSolutions(self._leaf_ids, range(self._n_leaves), uc)
+        else:
+            st.scratch = {"g": g}
+        return st
+
+    def solve_device(self, f: torch.Tensor, g: torch.Tensor) -> dict:
+        """Multi-RHS solve with device-resident inputs/outputs (no host round trip).
+
+        f: (nrhs, |root ext|) or (|root ext|, nrhs) handled as (rows, nrhs) after transpose;
+        g: (n_leaves, m, nrhs) interior loads in leaf-row order. Returns views into the pool:
+        u (N_gauss, nrhs), w, uc (n_leaves, P, nrhs), h_root.
+        """
+        nrhs = g.shape[-1]
+        prog = self._program(nrhs)
+        self._run(prog, f.reshape(-1, nrhs), g.reshape(-1, nrhs))
+        lay, pool, N = self._layout, prog["pool"], self.plan.n_gauss
+        P = self.p ** 2
+        return {"u": pool[lay["U"]:lay["U"] + N], "w": pool[lay["W"]:lay["W"] + N],
+                "uc": pool[lay["UC"]:lay["UC"] + self._n_leaves * P].view(self._n_leaves, P, nrhs),
+                "g": pool[lay["G"]:lay["G"] + self._n_leaves * (self.p - 2) ** 2]}
+
+    # -- sweep program ----------------------------------------------------------------------
+    def _run(self, prog, fdev, gdev, down=True):
+        lib = _ext.load()
+        pool = prog["pool"]
+        lay = self._layout
+        N = self.plan.n_gauss
+        s = _stream_ptr()
+        pool[lay["U"]:lay["U"] + 2 * N].zero_()
+        pool[lay["G"]:lay["G"] + gdev.shape[0]].copy_(gdev)
+        for step in prog["up"]:
+            _ext.check(lib.hps_sweep_gemv(step, s), "upward sweep")
+        if not down:
+            return
+        pool.index_copy_(0, prog["root_rows"], fdev)
+        for step in prog["down"]:
+            _ext.check(lib.hps_sweep_gemv(step, s), "downward sweep")
+
+    def _program(self, nrhs):
+        prog = self._sweeps.get(nrhs)
+        if prog is not None:
+            return prog
+        lay = self._layout
+        pool = torch.zeros((lay["rows"], nrhs), dtype=torch.float64, device=self.device)
+        keep = []
+
+        def gemv(nitems, R, K, A, xidx, oidx, x2idx=None, aidx=None):
+            xi = _i32(xidx, self.device)
+            oi = _i32(oidx, self.device)
+            x2 = None if x2idx is None else _i32(x2idx, self.device)
+            ai = None if aidx is None else _i32(aidx, self.device)
+            keep.extend([xi, oi, x2, ai])
+            return _ext.GemvBatch(nitems, R, K, nrhs, A, pool.data_ptr(), xi.data_ptr(), _ext.ptr(x2),
+                                  _ext.ptr(ai), oi.data_ptr())
+
+        up, down = [], []
+        p, q = self.p, self.q
+        m, b, P, c = (p - 2) ** 2, 4 * q, p * p, 4 * (p - 1)
+        hslot = lay["hslot"]
+        tree, plan = self.tree, self.plan
+        # leaves: h = H g
+        for grp in self.leaf_groups:
+            L = len(grp.ids)
+            rows = grp.first_row + np.arange(L)
+            xidx = lay["G"] + rows[:, None] * m + np.arange(m)[None, :]
+            oidx = np.stack([hslot[n] + np.arange(b) for n in grp.ids])
+            up.append(gemv(L, b, m, _ext.mat(grp.h, b * m, m), xidx, oidx))
+        # parents, deepest first
+        for grp in sorted(self.parent_groups, key=lambda g_: -g_.depth):
+            m3, e, n1 = grp.m3, grp.e, grp.n1
+            xw, x2w, ow, ah, oh = [], [], [], [], []
+            for nid in grp.ids:
+                ca, cb = tree.nodes[nid].children
+                en = plan.node[nid]
+                xw.append(hslot[cb] + en.pos3_b)
+                x2w.append(hslot[ca] + en.pos3_a)
+                ow.append(lay["W"] + en.j3)
+                ah.append(np.concatenate([hslot[ca] + en.pos1_a, hslot[cb] + en.pos2_b]))
+                oh.append((lay["hpre"][nid] if grp.wrap is not None else hslot[nid]) + np.arange(e))
+            nI = len(grp.ids)
+            if grp.wrap is not None:
+                ldx = m3 + grp.wrap["ec"]
+                xmat = _ext.mat(grp.wrap["xsw"], m3 * ldx, ldx)
+            else:
+                xmat = _ext.mat(grp.xs, m3 * (m3 + e), m3 + e)
+            up.append(gemv(nI, m3, m3, xmat, np.stack(xw), np.stack(ow), x2idx=np.stack(x2w)))
+            up.append(gemv(nI, e, m3, _ext.mat(grp.tei, e * m3, m3), np.stack(ow), np.stack(oh), aidx=np.stack(ah)))
+            if grp.wrap is not None:
+                nid = grp.ids[0]
+                ec = grp.wrap["ec"]
+                up.append(gemv(1, ec, e, _ext.mat(grp.wrap["qd_dev"], 0, e),
+                               (lay["hpre"][nid] + np.arange(e))[None], (hslot[nid] + np.arange(ec))[None]))
+        # downward: parents root first
+        for grp in sorted(self.parent_groups, key=lambda g_: g_.depth):
+            m3, e = grp.m3, grp.e
+            if grp.wrap is not None:
+                nid = grp.ids[0]
+                en = plan.node[nid]
+                ec = grp.wrap["ec"]
+                ext = lay["U"] + en.ext
+                down.append(gemv(1, e, ec, _ext.mat(grp.wrap["pu_dev"], 0, ec), ext[None],
+                                 (lay["U"] + en.wrap.fine)[None]))
+                down.append(gemv(1, m3, ec, _ext.mat(grp.wrap["xsw"], m3 * (m3 + ec), m3 + ec, off=m3),
+                                 ext[None], (lay["U"] + en.j3)[None], aidx=(lay["W"] + en.j3)[None]))
+                continue
+            xi = np.stack([lay["U"] + plan.node[n].ext_mergeorder for n in grp.ids])
+            j3 = np.stack([plan.node[n].j3 for n in grp.ids])
+            down.append(gemv(len(grp.ids), m3, e, _ext.mat(grp.xs, m3 * (m3 + e), m3 + e, off=m3), xi,
+                             lay["U"] + j3, aidx=lay["W"] + j3))
+        # leaves: u_c[i_ci] = [F | S] [g; u_ext],  u_c[i_ce] = L u_ext
+        for grp in self.leaf_groups:
+            L = len(grp.ids)
+            rows = grp.first_row + np.arange(L)
+            ext = np.stack([lay["U"] + plan.node[n].ext for n in grp.ids])
+            gx = lay["G"] + rows[:, None] * m + np.arange(m)[None, :]
+            base = lay["UC"] + rows[:, None] * P
+            down.append(gemv(L, m, m + b, _ext.mat(grp.fs, m * (m + b), m + b), np.concatenate([gx, ext], axis=1),
+                             base + grp.sc.i_ci[None, :]))
+            down.append(gemv(L, c, b, _ext.mat(grp.consts["lift"], 0, b), ext, base + grp.sc.i_ce[None, :]))
+        root_rows = torch.as_tensor(lay["U"] + plan.node[tree.root].ext, dtype=torch.long, device=self.device)
+        prog = {"pool": pool, "up": up, "down": down, "keep": keep, "root_rows": root_rows}
+        self._sweeps[nrhs] = prog
+        return prog
+
+
+# ------------------------------------------------------------------------------------------
+# build stage
+
+
+def _check_order(tree, order):
+    n = len(tree.nodes)
+    if order is None:
+        return list(range(n - 1, -1, -1))
+    order = [int(i) for i in order]
+    if sorted(order) != list(range(n)):
+        raise ValueError("order must be a permutation of the node ids")
+    done = set()
+    for nid in order:
+        node = tree.nodes[nid]
+        if not node.is_leaf and not all(c in done for c in node.children):
+            raise ValueError(f"order processes box {nid} before its children")
+        done.add(nid)
+    return order
+
+
+def _depths(tree):
+    depth = {tree.root: 0}
+    stack = [tree.root]
+    while stack:
+        nid = stack.pop()
+        for c in tree.nodes[nid].children:
+            depth[c] = depth[nid] + 1
+            stack.append(c)
+    return depth
+
+
+def _wrap_dense(wrap, q):
+    """P_up / P_down (block diagonal, reference solver.py:157-174) for one wrap plan."""
+    up_ref, down_ref = edge_interpolators(q)
+    rows = cols = 0
+    blocks = []
+    for blk in wrap.blocks:
+        if blk[0] == "identity":
+            u = d = np.eye(blk[1])
+        else:
+            u, d = up_ref, down_ref
+        blocks.append((u, d))
+        rows += u.shape[0]
+        cols += u.shape[1]
+    pu, pd = np.zeros((rows, cols)), np.zeros((cols, rows))
+    r = c = 0
+    for u, d in blocks:
+        pu[r:r + u.shape[0], c:c + u.shape[1]] = u
+        pd[c:c + d.shape[0], r:r + d.shape[1]] = d
+        r += u.shape[0]
+        c += u.shape[1]
+    return pu, pd
+
+
+def build_stage(tree, spec, p: int, q: int, mode: str = "stored", plan=None, order=None) -> FactorizedSolver:
+    """Children-first build of all operators on the GPU (reference solver.py:357-415)."""
+    global BUILD_COUNT
+    if mode not in ("stored", "econ"):
+        raise ValueError(f"unknown mode {mode!r}")
+    if p < q + 1:
+        raise ValueError(f"leaf order must satisfy p >= q+1, got p={p}, q={q}")
+    if mode == "econ":
+        raise NotImplementedError("economy mode is not implemented on the GPU path yet")
+    t0 = time.perf_counter()
+    if plan is None:
+        plan = enumerate_gauss_nodes(tree, q)
+    rng_pts = np.stack([np.linspace(0.05, 0.95, 13), np.linspace(0.1, 0.9, 13)], axis=1)
+    rb = tree.nodes[tree.root].bounds
+    sample = np.column_stack([rb.x1lo + rng_pts[:, 0] * rb.width, rb.x2lo + rng_pts[:, 1] * rb.height])
+    spec.coefficients.check_ellipticity(sample, label=spec.name)
+    order = _check_order(tree, order)
+    solver = FactorizedSolver(tree, plan, spec, p, q, mode)
+    _build_device(solver, order)
+    solver.build_seconds = time.perf_counter() - t0
+    BUILD_COUNT += 1
+    return solver
+
+
+def _build_device(solver: FactorizedSolver, order):
+    lib = _ext.load()
+    dev = solver.device
+    tree, plan, spec, p, q = solver.tree, solver.plan, solver.spec, solver.p, solver.q
+    m, b, c, P = (p - 2) ** 2, 4 * q, 4 * (p - 1), p * p
+    s = _stream_ptr()
+
+    # ---- leaf stage: one hps_leaf_build per leaf shape
+    groups: dict = {}
+    for nid in range(len(tree.nodes)):
+        node = tree.nodes[nid]
+        if node.is_leaf:
+            key = (node.bounds.x1hi - node.bounds.x1lo, node.bounds.x2hi - node.bounds.x2lo)
+            groups.setdefault(key, []).append(nid)
+    tloc = {}          # node id -> (tensor, element offset, ld)
+    row = 0
+    leaf_ids = []
+    for key, ids in groups.items():
+        sc = shape_constants(p, q, float(key[0]), float(key[1]))
+        grp = _LeafGroup(key, ids, sc, first_row=row)
+        L = len(ids)
+        row += L
+        leaf_ids.extend(ids)
+        int_pos = np.full(P, -1)
+        int_pos[sc.i_ci] = np.arange(m)
+        ext_pos = np.full(P, -1)
+        ext_pos[sc.i_ce] = np.arange(c)
+        grp.consts = {"dx": _f64(sc.dx, dev), "dy": _f64(sc.dy, dev), "dxx": _f64(sc.dxx, dev),
+                      "dyy": _f64(sc.dyy, dev), "int_pos": _i32(int_pos, dev), "ext_pos": _i32(ext_pos, dev),
+                      "lift": _f64(sc.lift, dev), "dfi": _f64(sc.dfi, dev), "t0": _f64(sc.t0, dev)}
+        org = torch.as_tensor(np.array([[tree.nodes[n].bounds.x1lo, tree.nodes[n].bounds.x2lo] for n in ids]),
+                              dtype=torch.float64, device=dev)
+        pts0 = torch.as_tensor(sc.cheb2d(), dtype=torch.float64, device=dev)
+        pts = pts0[None, :, :] + org[:, None, :]
+        coef = coeff_mod.evaluate(spec.coefficients, pts).contiguous()
+        if not bool(torch.isfinite(coef).all()):
+            bad = int(torch.nonzero(~torch.isfinite(coef).all(dim=0).all(dim=1))[0, 0])
+            bnd = tree.nodes[ids[bad]].bounds
+            raise ValueError(f"non-finite coefficient evaluation on leaf "
+                             f"{(bnd.x1lo, bnd.x1hi, bnd.x2lo, bnd.x2hi)}")
+        grp.fs = torch.empty((L, m, m + b), dtype=torch.float64, device=dev)
+        grp.h = torch.empty((L, b, m), dtype=torch.float64, device=dev)
+        t_maps = torch.empty((L, b, b), dtype=torch.float64, device=dev)
+        grp.anorm = torch.empty(L, dtype=torch.float64, device=dev)
+        grp.ainvnorm = torch.empty(L, dtype=torch.float64, device=dev)
+        grp.status = torch.zeros(L, dtype=torch.int32, device=dev)
+        ws = torch.empty(int(lib.hps_leaf_workspace_bytes(L, p, q)), dtype=torch.uint8, device=dev)
+        cs = grp.consts
+        lb = _ext.LeafBatch(L, p, q, coef.data_ptr(), cs["dx"].data_ptr(), cs["dy"].data_ptr(),
+                            cs["dxx"].data_ptr(), cs["dyy"].data_ptr(), cs["int_pos"].data_ptr(),
+                            cs["ext_pos"].data_ptr(), cs["lift"].data_ptr(), cs["dfi"].data_ptr(),
+                            cs["t0"].data_ptr(), grp.fs.data_ptr(), grp.h.data_ptr(), t_maps.data_ptr(),
+                            grp.anorm.data_ptr(), grp.ainvnorm.data_ptr(), grp.status.data_ptr(), ws.data_ptr())
+        _ext.check(lib.hps_leaf_build(lb, s), "leaf build")
+        for slot, nid in enumerate(ids):
+            tloc[nid] = (t_maps, slot * b * b, b)
+            solver.leaf_loc[nid] = (len(solver.leaf_groups), slot)
+        solver.leaf_groups.append(grp)
+    solver._leaf_ids = leaf_ids
+    solver._n_leaves = len(leaf_ids)
+
+    # ---- merge stage: depth by depth, one hps_merge_build per interface shape
+    depth = _depths(tree)
+    solver.depth = depth
+    parents = [n for n in range(len(tree.nodes)) if not tree.nodes[n].is_leaf]
+    by_depth: dict = {}
+    for nid in parents:
+        by_depth.setdefault(depth[nid], []).append(nid)
+    for d in sorted(by_depth, reverse=True):
+        sig_groups: dict = {}
+        for nid in by_depth[d]:
+            en = plan.node[nid]
+            ca, cb = tree.nodes[nid].children
+            if en.wrap is not None:
+                sig = ("wrap", nid)
+            else:
+                sig = (en.j3.size, en.pos1_a.size, en.pos2_b.size, tloc[ca][2], tloc[cb][2])
+            sig_groups.setdefault(sig, []).append(nid)
+        for sig, ids in sig_groups.items():
+            en0 = plan.node[ids[0]]
+            ca0, cb0 = tree.nodes[ids[0]].children
+            grp = _ParentGroup(d, ids, en0.j3.size, en0.pos1_a.size, en0.pos2_b.size, tloc[ca0][2], tloc[cb0][2])
+            npar, m3, e = len(ids), grp.m3, grp.e
+            ta = [tloc[tree.nodes[n].children[0]] for n in ids]
+            tb = [tloc[tree.nodes[n].children[1]] for n in ids]
+            ta_ptr = _ptr_array([t.data_ptr() + 8 * off for t, off, _ in ta], dev)
+            tb_ptr = _ptr_array([t.data_ptr() + 8 * off for t, off, _ in tb], dev)
+            rows_idx = [np.concatenate([plan.node[n].pos1_a, plan.node[n].pos3_a, plan.node[n].pos2_b,
+                                        plan.node[n].pos3_b]) for n in ids]
+            same = all(np.array_equal(rows_idx[0], r) for r in rows_idx[1:])
+            idx = _i32(rows_idx[0] if same else np.stack(rows_idx), dev)
+            grp.xs = torch.empty((npar, m3, m3 + e), dtype=torch.float64, device=dev)
+            grp.tei = torch.empty((npar, e, m3), dtype=torch.float64, device=dev)
+            grp.tnew = torch.empty((npar, e, e), dtype=torch.float64, device=dev)
+            grp.dnorm = torch.empty(npar, dtype=torch.float64, device=dev)
+            grp.xnorm = torch.empty(npar, dtype=torch.float64, device=dev)
+            grp.status = torch.zeros(npar, dtype=torch.int32, device=dev)
+            ws = torch.empty(int(lib.hps_merge_workspace_bytes(npar, m3, e)), dtype=torch.uint8, device=dev)
+            mb = _ext.MergeBatch(npar, m3, grp.n1, grp.n2, ta_ptr.data_ptr(), tb_ptr.data_ptr(), grp.lda, grp.ldb,
+                                 idx.data_ptr(), 0 if same else idx.shape[1], grp.xs.data_ptr(),
+                                 grp.tei.data_ptr(), grp.tnew.data_ptr(), grp.dnorm.data_ptr(),
+                                 grp.xnorm.data_ptr(), grp.status.data_ptr(), ws.data_ptr())
+            _ext.check(lib.hps_merge_build(mb, s), "merge build")
+            if en0.wrap is not None:
+                _apply_wrap(solver, grp, plan.node[ids[0]], lib, s)
+                tloc[ids[0]] = (grp.wrap.pop("tw"), 0, grp.wrap["ec"])
+            else:
+                for slot, nid in enumerate(ids):
+                    tloc[nid] = (grp.tnew, slot * e * e, e)
+            grp.tnew = None   # tloc holds the DtN maps until the grandparent consumes them
+            solver.parent_groups.append(grp)
+        # children's DtN maps are consumed: drop them (stream-ordered reuse by the allocator)
+        for nid in by_depth[d]:
+            for ch in tree.nodes[nid].children:
+                tloc.pop(ch, None)
+    tloc.clear()
+    _finish_checks(solver, order)
+    solver._layout = _layout(solver)
+
+
+def _apply_wrap(solver, grp, en, lib, s):
+    """Re-express a refined parent on the coarse grid (reference solver.py:177-188):
+    T <- P_down T[perm,perm] P_up,  S <- S[:,perm] P_up, via Qd = P_down Pi, Qu = Pi^T P_up."""
+    dev = solver.device
+    pu, pd = _wrap_dense(en.wrap, solver.q)
+    perm = en.wrap.perm
+    e, m3 = grp.e, grp.m3
+    ec = pu.shape[1]
+    qd = np.zeros((ec, e))
+    qd[:, perm] = pd
+    qu = np.zeros((e, ec))
+    qu[perm, :] = pu
+    qd_t, qu_t, pu_t = _f64(qd, dev), _f64(qu, dev), _f64(pu, dev)
+    tmp = torch.empty((ec, e), dtype=torch.float64, device=dev)
+    tw = torch.empty((ec, ec), dtype=torch.float64, device=dev)
+    xsw = torch.empty((m3, m3 + ec), dtype=torch.float64, device=dev)
+    xsw[:, :m3].copy_(grp.xs[0, :, :m3])
+
+    def gemm(M, N, K, A, B, C):
+        _ext.check(lib.hps_gemm_batched(1, M, N, K, 1.0, A, B, 0.0, C, None, 0, s), "wrap gemm")
+
+    gemm(ec, e, e, _ext.mat(qd_t, 0, e), _ext.mat(grp.tnew, 0, e), _ext.mat(tmp, 0, e))
+    gemm(ec, ec, e, _ext.mat(tmp, 0, e), _ext.mat(qu_t, 0, ec), _ext.mat(tw, 0, ec))
+    gemm(m3, ec, e, _ext.mat(grp.xs, 0, m3 + e, off=m3), _ext.mat(qu_t, 0, ec), _ext.mat(xsw, 0, m3 + ec, off=m3))
+    grp.wrap = {"pu": pu, "pd": pd, "ec": ec, "qd_dev": qd_t, "pu_dev": pu_t, "xsw": xsw, "tw": tw}
+    grp.xs = None  # the retained operator is xsw = [X | S P_up]
+
+
+def _finish_checks(solver, order):
+    """Sync once and apply the reference's rcond < 1e-13 rule with exact 1-norm condition
+    numbers (leaf.py:104-121, solver.py:108-119). The failing node reported is the first
+    one in the build order, as in the reference's sequential sweep."""
+    bad = {}
+    for grp in solver.leaf_groups:
+        an, ai, st = grp.anorm.cpu().numpy(), grp.ainvnorm.cpu().numpy(), grp.status.cpu().numpy()
+        for slot, nid in enumerate(grp.ids):
+            rc = _rcond(an[slot], ai[slot], st[slot])
+            if not (np.isfinite(rc) and rc >= RCOND_FLOOR):
+                bad[nid] = ("leaf", rc)
+    for grp in solver.parent_groups:
+        an, ai, st = grp.dnorm.cpu().numpy(), grp.xnorm.cpu().numpy(), grp.status.cpu().numpy()
+        for slot, nid in enumerate(grp.ids):
+            rc = _rcond(an[slot], ai[slot], st[slot])
+            if not (np.isfinite(rc) and rc >= RCOND_FLOOR):
+                bad[nid] = ("merge", rc)
+    solver.rcond_min = None
+    if not bad:
+        return
+    for nid in order:
+        if nid in bad:
+            kind, rc = bad[nid]
+            cond = math.inf if (rc == 0 or not np.isfinite(rc)) else 1.0 / max(rc, np.finfo(float).tiny)
+            if kind == "leaf":
+                raise LeafSingularError(f"interior collocation block of leaf {nid} is numerically singular "
+                                        f"(condition estimate {cond:.2e})")
+            raise MergeSingularError(f"interface operator of box {nid} is numerically singular "
+                                     f"(condition estimate {cond:.2e}); the merged box has an "
+                                     "interface resonance")
+
+
+def _rcond(anorm, ainvnorm, status):
+    if status != 0 or anorm == 0 or not np.isfinite(anorm) or not np.isfinite(ainvnorm):
+        return 0.0
+    return 1.0 / (anorm * ainvnorm)
+
+
+def _layout(solver):
+    """Pool rows for the sweeps: U | W | h slots (+ pre-wrap slots) | G | UC."""
+    tree, plan = solver.tree, solver.plan
+    N = plan.n_gauss
+    lay = {"U": 0, "W": N}
+    cur = 2 * N
+    hslot, hsize, hpre = {}, {}, {}
+    wrapped = {g.ids[0]: g for g in solver.parent_groups if g.wrap is not None}
+    for nid in range(len(tree.nodes)):
+        size = plan.node[nid].ext.size
+        hslot[nid], hsize[nid] = cur, size
+        cur += size
+        if nid in wrapped:
+            hpre[nid] = cur
+            cur += wrapped[nid].e
+    m = (solver.p - 2) ** 2
+    lay["G"] = cur
+    cur += solver._n_leaves * m
+    lay["UC"] = cur
+    cur += solver._n_leaves * solver.p ** 2
+    lay.update(rows=cur, hslot=hslot, hsize=hsize, hpre=hpre)
+    return lay
+
+
+def upward_pass(solver: FactorizedSolver, g=None) -> SolveState:
+    """Upward pass only (reference solver.py:418-425): h_root and w are set, u is zero."""
+    return solver._solve_host(None, g, down=False)
+
+
+def downward_pass(solver: FactorizedSolver, f, state: SolveState) -> SolveState:
+    """Complete a state from upward_pass with Dirichlet data f (reference solver.py:428-432).
+    The device program re-runs the (deterministic) upward sweep with the same load."""
+    g = state.scratch.get("g") if state.scratch else None
+    full = solver._solve_host(f, g, down=True)
+    full.scratch = None
+    return full
+
+
+def solve(solver: FactorizedSolver, f=None, g=None) -> SolveState:
+    return solver.solve(f, g)

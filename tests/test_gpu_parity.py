@@ -1,0 +1,125 @@
+"""GPU build/solve (through build_stage -> C ABI) vs the pinned CPU oracle and the golden
+vectors produced by the reference. Tolerances: relative max-norm <= 1e-10 (<= 1e-9 at
+p >= 32), as BASELINE.json's north star states."""
+import numpy as np
+import pytest
+
+from hps_testutil import golden, rel_maxdiff
+from oracle import hps_oracle as orc
+from paper_1612_02736_b200 import (LeafSingularError, build_balanced_refined_tree, build_stage, build_uniform_tree,
+                                   catalog, enumerate_gauss_nodes, problems, refine_near_point)
+
+pytestmark = pytest.mark.gpu
+UNIT = (0.0, 1.0, 0.0, 1.0)
+
+
+def _compare_fixture(fx, st, tol, prefix=""):
+    ids = fx[prefix + "leaf_ids"]
+    sol = np.stack([st.leaf_solutions[int(i)] for i in ids])
+    assert rel_maxdiff(sol, fx[prefix + "leaf_sol"]) <= tol
+    assert rel_maxdiff(st.u, fx[prefix + "u"]) <= tol
+
+
+def test_config1_vs_golden_and_oracle():
+    fx = golden("cfg1.npz")
+    tree = build_uniform_tree(UNIT, 4)
+    spec = problems.config1_spec()
+    solver = build_stage(tree, spec, 16, 15)
+    st = solver.solve()
+    _compare_fixture(fx, st, 1e-10)
+    assert rel_maxdiff(st.h_root, fx["h_root"]) <= 1e-10 or np.abs(fx["h_root"]).max() == 0
+    # random-RHS variant (8 Gaussians, f = 0)
+    st2 = solver.solve(f=lambda pts: np.zeros(len(pts)), g=problems.config1_random_load(0))
+    _compare_fixture(fx, st2, 1e-10, prefix="rand_")
+    # error vs the exact solution within 2x of the reference's
+    exact = spec.u_exact
+    err = 0.0
+    for lf in tree.leaves():
+        pts = orc.leaf_points(lf.bounds, 16, 15)
+        geo = orc.leaf_geometry(16, 15, lf.bounds.width, lf.bounds.height)
+        err = max(err, np.abs(st.leaf_solutions[lf.id][geo["i_ce"]] - exact(pts[geo["i_ce"]])).max())
+    assert err <= 2.0 * fx["linf_error"][0] + 1e-15
+
+
+def test_config2_small_vs_golden():
+    fx = golden("cfg2_n4.npz")
+    spec = problems.config2_spec()
+    st = build_stage(build_uniform_tree(UNIT, 4), spec, 16, 15).solve()
+    _compare_fixture(fx, st, 1e-10)
+
+
+def test_config3_small_vs_golden():
+    fx = golden("cfg3_n4.npz")
+    st = build_stage(build_uniform_tree(UNIT, 4), problems.config3_spec(), 32, 31).solve()
+    _compare_fixture(fx, st, 1e-9)
+
+
+def test_config4_small_vs_golden():
+    fx = golden("cfg4_small.npz")
+    tree = build_balanced_refined_tree(4, (0.3, 0.7), 3)
+    st = build_stage(tree, problems.config4_spec(), 16, 14).solve()
+    _compare_fixture(fx, st, 1e-10)
+
+
+def test_refined_reference_native_vs_golden():
+    fx = golden("refined_r4.npz")
+    tree = build_uniform_tree(UNIT, 4)
+    refine_near_point(tree, (0.5, 0.5), 1)
+    st = build_stage(tree, catalog("manufactured", u="sin(pi*x1)*sin(pi*x2)"), 9, 8).solve()
+    _compare_fixture(fx, st, 1e-10)
+
+
+def test_config5_small_backward_euler_vs_golden():
+    fx = golden("cfg5_n4.npz")
+    dt = 1e-3
+    tree = build_uniform_tree(UNIT, 4)
+    solver = build_stage(tree, problems.config5_spec(dt), 16, 15)
+    for r in range(2):
+        u0 = problems.config5_initial(r)
+        tabs = {lf.id: u0(orc.leaf_points(lf.bounds, 16, 15)) for lf in tree.leaves()}
+        for step in (1, 2):
+            t = step * dt
+            st = solver.solve(f=lambda pts, _t=t: problems.config5_dirichlet(pts, _t),
+                              g=orc.be_loads(tabs, tree, 16, 15, dt))
+            tabs = st.leaf_solutions
+        sol = np.stack([tabs[i] for i in sorted(tabs)])
+        assert rel_maxdiff(sol, fx[f"rhs{r}_leaf_sol"]) <= 1e-10
+
+
+@pytest.mark.parametrize("n,p,q", [(2, 9, 8), (4, 12, 11), (8, 16, 15)])
+def test_varcoef_vs_oracle(n, p, q):
+    spec = catalog("varcoef_helmholtz", kappa=10.0)
+    tree = build_uniform_tree(UNIT, n)
+    solver = build_stage(tree, spec, p, q)
+    f = lambda pts: np.sin(2 * pts[:, 0] + pts[:, 1])
+    st = solver.solve(f=f)
+    ref = orc.solve(orc.build(tree, spec, p, q, enumerate_gauss_nodes(tree, q)), f)
+    sol = np.stack([st.leaf_solutions[i] for i in sorted(ref["leaf_solutions"])])
+    rsol = np.stack([ref["leaf_solutions"][i] for i in sorted(ref["leaf_solutions"])])
+    assert rel_maxdiff(sol, rsol) <= 1e-10
+    assert rel_maxdiff(st.u, ref["u"]) <= 1e-10
+    assert rel_maxdiff(st.w, ref["w"]) <= 1e-10
+
+
+def test_harmonic_reproduction_and_boundary_exact():
+    tree = build_uniform_tree(UNIT, 4)
+    solver = build_stage(tree, catalog("laplace"), 9, 8)
+    f = lambda pts: np.cos(3 * pts[:, 0]) + pts[:, 1]
+    st = solver.solve(f=f)
+    ext = solver.plan.root_exterior()
+    np.testing.assert_array_equal(st.u[ext], f(solver.plan.coords[ext]))
+    st = solver.solve(f=lambda pts: pts[:, 0])
+    for lf in tree.leaves():
+        pts = orc.leaf_points(lf.bounds, 9, 8)
+        assert np.abs(st.leaf_solutions[lf.id] - pts[:, 0]).max() <= 1e-11
+
+
+def test_zero_data_zero_solution():
+    solver = build_stage(build_uniform_tree(UNIT, 2), catalog("laplace"), 9, 8)
+    assert np.abs(solver.solve().u).max() == 0.0
+
+
+def test_resonant_leaf_raises():
+    tree = build_uniform_tree(UNIT, 1)
+    with pytest.raises(LeafSingularError, match="singular"):
+        build_stage(tree, catalog("helmholtz", kappa=np.sqrt(2.0) * np.pi), 20, 19)
