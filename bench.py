@@ -1,0 +1,416 @@
+"""HPS build/solve benchmark (BASELINE.json metric) — one JSON line on rank 0.
+
+Default workload = BASELINE.json configs[1] (config 2): variable-coefficient elliptic
+problem on [0,1]^2, 64x64 leaves, p=16, q=15, N_cheb = 923,521, FP64.
+
+  step   = one solve (upward + downward sweep, reference solver.py:337-354) of one batch of
+           nrhs right-hand sides against the operators built once by build_stage
+  value  = solve Mpts/s per RHS = N_cheb * nrhs / (seconds per step) / 1e6, whole job
+           (summed over ranks), inputs resident in HBM
+  e2e    = the same metric through the reference-facing API FactorizedSolver.solve(f, g)
+           with host numpy inputs / outputs (H2D of f,g and D2H of u, w, h, leaf
+           tabulations inside the timed region)
+  build  = build_stage seconds, canonical FP64 TFLOP/s and fraction of the measured
+           37.1 TFLOP/s DMMA peak (profiles/fp64_peaks_r01.jsonl)
+
+--impl reference times the CPU oracle port (oracle/hps_oracle.py, a restatement of the
+reference's numpy/scipy path) on the host cores with the same config/metric.
+Multi-GPU (--gpus N under torchrun): independent replicas over disjoint RHS batches
+(SURVEY.md 8e "data-parallel over RHS"), no data-path collective; timing max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.1     # measured DMMA m8n8k4 peak on this pool's B200 (tools/fp64_peaks.cu)
+UNIT = (0.0, 1.0, 0.0, 1.0)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def make_config(cfg: int, n_override: int = 0):
+    from paper_1612_02736_b200 import build_balanced_refined_tree, build_uniform_tree, problems
+    if cfg == 1:
+        return build_uniform_tree(UNIT, n_override or 4), problems.config1_spec(), 16, 15, "config1: Poisson 4x4 p=16"
+    if cfg == 2:
+        n = n_override or 64
+        return (build_uniform_tree(UNIT, n), problems.config2_spec(), 16, 15,
+                f"config2: var-coef elliptic {n}x{n} leaves p=16 q=15")
+    if cfg == 3:
+        n = n_override or 32
+        return (build_uniform_tree(UNIT, n), problems.config3_spec(), 32, 31,
+                f"config3: Helmholtz kappa=80 {n}x{n} leaves p=32 q=31")
+    if cfg == 4:
+        return (build_balanced_refined_tree(8, (0.3, 0.7), 8), problems.config4_spec(), 16, 14,
+                "config4: 2:1-balanced refined quadtree (175 leaves) p=16 q=14")
+    n = n_override or 128
+    return (build_uniform_tree(UNIT, n), problems.config5_spec(1e-3), 16, 15,
+            f"config5: backward-Euler heat {n}x{n} leaves p=16 q=15")
+
+
+def canonical_build_flops(tree, plan, p, q):
+    """leaf (2/3+4/3)m^3 + 2mcb + 2m^2b + 2bPb + 2bm^2; merge (2/3)m3^3 + 2m3^2 e + 2e^2 m3."""
+    m, b, c, P = (p - 2) ** 2, 4 * q, 4 * (p - 1), p * p
+    nleaf = sum(1 for n in tree.nodes if n.is_leaf)
+    leaf = nleaf * (2.0 * m ** 3 + 2.0 * m * c * b + 2.0 * m * m * b + 2.0 * b * P * b + 2.0 * b * m * m)
+    merge = 0.0
+    for nid, node in enumerate(tree.nodes):
+        if node.is_leaf:
+            continue
+        en = plan.node[nid]
+        m3, e = en.j3.size, en.ext_mergeorder.size
+        merge += (2.0 / 3.0) * m3 ** 3 + 2.0 * m3 * m3 * e + 2.0 * e * e * m3
+        if en.wrap is not None:
+            ec = en.ext.size
+            merge += 2.0 * e * e * ec + 2.0 * ec * e * ec + 2.0 * m3 * e * ec
+    return leaf, merge
+
+
+def solve_bytes(tree, plan, p, q, nrhs):
+    """Canonical retained-operator bytes + vector bytes per solve."""
+    m, b, P = (p - 2) ** 2, 4 * q, p * p
+    nleaf = sum(1 for n in tree.nodes if n.is_leaf)
+    ops = nleaf * (m * b + m * m + b * m)
+    vec = nleaf * (m + P) * nrhs
+    for nid, node in enumerate(tree.nodes):
+        if node.is_leaf:
+            continue
+        en = plan.node[nid]
+        m3, e, ec = en.j3.size, en.ext_mergeorder.size, en.ext.size
+        ops += m3 * m3 + m3 * ec + e * m3 + (2 * e * ec if en.wrap is not None else 0)
+        vec += (2 * m3 + e + ec) * nrhs
+    return 8.0 * ops, 8.0 * vec
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"hps_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 7:
+                    rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for k, nm in enumerate(names):
+                if r[3 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": float(rows[0][1]),
+                "samples": len(rows), "reasons": sorted(reasons)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if os.environ.get("HPS_BENCH_BACKEND", "nccl") == "nccl" else "gloo")
+    return rank, ws
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# --------------------------------------------------------------------------- CPU reference arm
+
+def cpu_solve_rate(tree, spec, p, q, plan, reps=1, threads=None):
+    """Oracle (reference numpy/scipy restatement) build + timed solves; returns (Mpts/s per RHS, build s)."""
+    from threadpoolctl import threadpool_limits
+    from oracle import hps_oracle as orc
+    from paper_1612_02736_b200.geometry import count_chebyshev_dofs
+    ncheb = count_chebyshev_dofs(tree, p)
+    with threadpool_limits(limits=threads):
+        t0 = time.perf_counter()
+        ops = orc.build(tree, spec, p, q, plan)
+        tb = time.perf_counter() - t0
+        root_ext = plan.node[tree.root].ext
+        f = np.asarray(spec.dirichlet(plan.coords[root_ext]) if spec.dirichlet else np.zeros(root_ext.size))
+        g = {}
+        for lf in tree.leaves():
+            geo = orc.leaf_geometry(p, q, lf.bounds.width, lf.bounds.height)
+            pts = orc.leaf_points(lf.bounds, p, q)[geo["i_ci"]]
+            g[lf.id] = spec.load(pts) if hasattr(spec, "load") else np.zeros(len(pts))
+        orc.solve(ops, f, g)
+        times = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            orc.solve(ops, f, g)
+            times.append(time.perf_counter() - t0)
+    ts = min(times)
+    return ncheb / ts / 1e6, tb, ts
+
+
+def best_threads(tree_small, spec, p, q):
+    from paper_1612_02736_b200.geometry import enumerate_gauss_nodes
+    plan = enumerate_gauss_nodes(tree_small, q)
+    best, best_t = None, None
+    for th in sorted({1, min(4, os.cpu_count() or 1), os.cpu_count() or 1}):
+        _, tb, ts = cpu_solve_rate(tree_small, spec, p, q, plan, reps=1, threads=th)
+        if best_t is None or tb + ts < best_t:
+            best, best_t = th, tb + ts
+    return best
+
+
+def run_reference(args, rank, ws):
+    if rank != 0:
+        return
+    from paper_1612_02736_b200.geometry import count_chebyshev_dofs, enumerate_gauss_nodes
+    tree, spec, p, q, desc = make_config(args.config, args.n)
+    small = make_config(args.config, 8 if args.config in (2, 5) else 4)[0] if args.config in (2, 3, 5) else tree
+    th = best_threads(small, spec, p, q)
+    plan = enumerate_gauss_nodes(tree, q)
+    from threadpoolctl import threadpool_limits
+    from oracle import hps_oracle as orc
+    ncheb = count_chebyshev_dofs(tree, p)
+    with threadpool_limits(limits=th):
+        t0 = time.perf_counter()
+        ops = orc.build(tree, spec, p, q, plan)
+        build_s = time.perf_counter() - t0
+        root_ext = plan.node[tree.root].ext
+        f = np.asarray(spec.dirichlet(plan.coords[root_ext]) if spec.dirichlet else np.zeros(root_ext.size))
+        g = {}
+        for lf in tree.leaves():
+            geo = orc.leaf_geometry(p, q, lf.bounds.width, lf.bounds.height)
+            g[lf.id] = spec.load(orc.leaf_points(lf.bounds, p, q)[geo["i_ci"]])
+        for _ in range(args.warmup):
+            orc.solve(ops, f, g)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            orc.solve(ops, f, g)
+        el = time.perf_counter() - t0
+    per = el / args.steps
+    val = ncheb * args.nrhs / (per * args.nrhs) / 1e6
+    lf, mf = canonical_build_flops(tree, plan, p, q)
+    line = {"impl": "reference", "metric": "HPS solve Mpts/s per RHS", "value": round(val, 4),
+            "unit": "Mpts/s per RHS", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(per * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded manufactured solution, SURVEY.md 8d)",
+            "config": {"workload": desc, "nrhs": 1, "N_cheb": ncheb},
+            "cpu_baseline": {"value": round(val, 4), "unit": "Mpts/s per RHS", "cores": th, "kind": "port",
+                             "sample": f"full workload; oracle/hps_oracle.py numpy/scipy, OPENBLAS threads={th} "
+                                       f"(best of a 1/4/nproc sweep), {args.steps} solves"},
+            "e2e": {"value": round(val, 4), "unit": "Mpts/s per RHS", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "build": {"seconds": round(build_s, 3), "tflops": round((lf + mf) / build_s / 1e12, 5)}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+
+def run_ours(args, rank, ws):
+    import torch
+    from paper_1612_02736_b200 import build_stage
+    from paper_1612_02736_b200.geometry import count_chebyshev_dofs, enumerate_gauss_nodes
+    from paper_1612_02736_b200 import _ext
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    hbm_peak, hbm_src = load_peaks()
+    tree, spec, p, q, desc = make_config(args.config, args.n)
+    plan = enumerate_gauss_nodes(tree, q)
+    ncheb = count_chebyshev_dofs(tree, p)
+    nrhs = args.nrhs
+    m, P = (p - 2) ** 2, p * p
+
+    # ---- build (warm once: first call pays lazy CUDA/module init)
+    build_stage(tree, spec, p, q, plan=plan)
+    torch.cuda.synchronize()
+    barrier(ws)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    solver = build_stage(tree, spec, p, q, plan=plan)
+    e1.record()
+    torch.cuda.synchronize()
+    build_wall = time.perf_counter() - t0
+    build_dev = e0.elapsed_time(e1) / 1e3
+    lf, mf = canonical_build_flops(tree, plan, p, q)
+    build_s = max_over_ranks(build_wall, ws)
+
+    # ---- device-resident inputs (seeded): f on the root boundary, g interior loads
+    rng = np.random.default_rng(1234 + rank)
+    root_ext = plan.node[tree.root].ext
+    f_host = np.asarray(spec.dirichlet(plan.coords[root_ext]) if spec.dirichlet else np.zeros(root_ext.size))
+    g_host = solver._leaf_table(None)
+    f_dev = torch.as_tensor(np.repeat(f_host[:, None], nrhs, axis=1) * (1.0 + 0.01 * rng.standard_normal(nrhs)),
+                            device="cuda").contiguous()
+    g_dev = torch.as_tensor(np.repeat(g_host.reshape(-1, 1), nrhs, axis=1), device="cuda").contiguous()
+    prog = solver._program(nrhs)
+    launches_per_step = len(prog["up"]) + len(prog["down"])
+
+    for _ in range(args.warmup):
+        solver.solve_device(f_dev, g_dev)
+    torch.cuda.synchronize()
+    barrier(ws)
+    with ClockSampler(local) as clk:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(args.steps):
+            solver.solve_device(f_dev, g_dev)
+        ev1.record()
+        torch.cuda.synchronize()
+        el = ev0.elapsed_time(ev1) / 1e3
+    el = max_over_ranks(el, ws)
+    per = el / args.steps
+    value = ncheb * nrhs * ws / per / 1e6
+
+    # ---- dominant kernel: leaf downward sweep ([F|S] [g; u_ext]), timed alone on the stream
+    lib = _ext.load()
+    sptr = torch.cuda.current_stream().cuda_stream
+    ngrp = len(solver.leaf_groups)
+    leaf_down = [st for st in prog["down"][-2 * ngrp:]][0::2]
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    k0.record()
+    for _ in range(reps):
+        for st in leaf_down:
+            lib.hps_sweep_gemv(st, sptr)
+    k1.record()
+    torch.cuda.synchronize()
+    kt = k0.elapsed_time(k1) / 1e3 / reps
+    nleaf = solver._n_leaves
+    b = 4 * q
+    kbytes = 8.0 * nleaf * (m * (m + b) + (m + b) * nrhs + m * nrhs)
+    achieved = kbytes / kt / 1e9
+
+    # ---- e2e through the public host API (host numpy in, host numpy out)
+    g_tab = solver._leaf_table(None)
+    e2e_steps = max(1, min(args.steps, 5))
+    solver.solve(f=f_host, g=g_tab)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        st = solver.solve(f=f_host, g=g_tab)
+    e2e_t = (time.perf_counter() - t0) / e2e_steps
+    e2e_t = max_over_ranks(e2e_t, ws)
+    lay = solver._layout
+    h2d = 8 * (root_ext.size + g_tab.size)
+    d2h = 8 * lay["rows"]
+
+    # ---- CPU baseline: oracle on a bounded sample (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.skip_cpu:
+        n_s = {1: 4, 2: 16, 3: 8, 4: 0, 5: 16}[args.config]
+        stree, sspec, _, _, sdesc = make_config(args.config, n_s) if n_s else (tree, spec, p, q, desc)
+        splan = enumerate_gauss_nodes(stree, q)
+        th = min(4, os.cpu_count() or 1)
+        rate, tb, ts = cpu_solve_rate(stree, sspec, p, q, splan, reps=3, threads=th)
+        cpu = {"value": round(rate, 4), "unit": "Mpts/s per RHS", "cores": th, "kind": "port",
+               "sample": f"{sdesc}: oracle build ({tb:.1f} s) + best of 3 solves ({ts * 1e3:.1f} ms), "
+                         f"OPENBLAS threads={th}"}
+
+    sb_ops, sb_vec = solve_bytes(tree, plan, p, q, nrhs)
+    line = {
+        "metric": "HPS solve Mpts/s per RHS", "value": round(value, 3), "unit": "Mpts/s per RHS",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(per * 1e3, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded manufactured solution / loads, SURVEY.md 8d; no dataset)",
+        "config": {"workload": desc, "nrhs": nrhs, "N_cheb": ncheb,
+                   "l2": "operators (%.2f GB) exceed the 126 MB L2; no flush needed" % (sb_ops / 1e9),
+                   "parallelism": f"replicas over RHS x{ws}" if ws > 1 else "1 GPU"},
+        "roofline": {"bound": "hbm", "kernel": "gemv_gather (leaf downward sweep)", "achieved": round(achieved, 1),
+                     "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                     "peak_source": hbm_src},
+        "solve_roofline": {"bytes_per_step": sb_ops + sb_vec, "achieved_gbs": round((sb_ops + sb_vec) / per / 1e9, 1),
+                           "frac": round((sb_ops + sb_vec) / per / 1e9 / hbm_peak, 4)},
+        "build": {"seconds": round(build_s, 4), "device_seconds": round(build_dev, 4),
+                  "gflop_canonical": round((lf + mf) / 1e9, 2),
+                  "tflops": round((lf + mf) / build_dev / 1e12, 3),
+                  "frac_fp64_peak": round((lf + mf) / build_dev / 1e12 / FP64_PEAK_TFLOPS, 4),
+                  "fp64_peak_tflops": FP64_PEAK_TFLOPS},
+        "e2e": {"value": round(ncheb * ws / e2e_t / 1e6, 3), "unit": "Mpts/s per RHS", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "cpu_baseline": cpu,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--n", type=int, default=0)
+    ap.add_argument("--nrhs", type=int, default=1)
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    rank, ws = dist_init()
+    if args.impl == "reference":
+        run_reference(args, rank, ws)
+    else:
+        run_ours(args, rank, ws)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -435,7 +435,8 @@ def _wrap_dense(wrap, q):
     return pu, pd
 
 
-def build_stage(tree, spec, p: int, q: int, mode: str = "stored", plan=None, order=None) -> FactorizedSolver:
+def build_stage(tree, spec, p: int, q: int, mode: str = "stored", plan=None, order=None,
+                profile: bool = False) -> FactorizedSolver:
     """Children-first build of all operators on the GPU (reference solver.py:357-415)."""
     global BUILD_COUNT
     if mode not in ("stored", "econ"):
@@ -453,14 +454,37 @@ def build_stage(tree, spec, p: int, q: int, mode: str = "stored", plan=None, ord
     spec.coefficients.check_ellipticity(sample, label=spec.name)
     order = _check_order(tree, order)
     solver = FactorizedSolver(tree, plan, spec, p, q, mode)
-    _build_device(solver, order)
+    _build_device(solver, order, profile)
     solver.build_seconds = time.perf_counter() - t0
     BUILD_COUNT += 1
     return solver
 
 
-def _build_device(solver: FactorizedSolver, order):
+class _Phases:
+    """Optional CUDA-event phase timing of the build (enabled by build_stage(..., profile=True))."""
+
+    def __init__(self, on):
+        self.on = on
+        self.marks = []
+
+    def mark(self, name):
+        if self.on:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.marks.append((name, ev))
+
+    def report(self):
+        if not self.on or len(self.marks) < 2:
+            return []
+        torch.cuda.synchronize()
+        return [(self.marks[i + 1][0], self.marks[i][1].elapsed_time(self.marks[i + 1][1]))
+                for i in range(len(self.marks) - 1)]
+
+
+def _build_device(solver: FactorizedSolver, order, profile=False):
     lib = _ext.load()
+    ph = _Phases(profile)
+    ph.mark("start")
     dev = solver.device
     tree, plan, spec, p, q = solver.tree, solver.plan, solver.spec, solver.p, solver.q
     m, b, c, P = (p - 2) ** 2, 4 * q, 4 * (p - 1), p * p
@@ -512,7 +536,9 @@ def _build_device(solver: FactorizedSolver, order):
                             cs["ext_pos"].data_ptr(), cs["lift"].data_ptr(), cs["dfi"].data_ptr(),
                             cs["t0"].data_ptr(), grp.fs.data_ptr(), grp.h.data_ptr(), t_maps.data_ptr(),
                             grp.anorm.data_ptr(), grp.ainvnorm.data_ptr(), grp.status.data_ptr(), ws.data_ptr())
+        ph.mark(f"leaf-prep {key}")
         _ext.check(lib.hps_leaf_build(lb, s), "leaf build")
+        ph.mark(f"leaf-build {key} x{L}")
         for slot, nid in enumerate(ids):
             tloc[nid] = (t_maps, slot * b * b, b)
             solver.leaf_loc[nid] = (len(solver.leaf_groups), slot)
@@ -561,7 +587,9 @@ def _build_device(solver: FactorizedSolver, order):
                                  idx.data_ptr(), 0 if same else idx.shape[1], grp.xs.data_ptr(),
                                  grp.tei.data_ptr(), grp.tnew.data_ptr(), grp.dnorm.data_ptr(),
                                  grp.xnorm.data_ptr(), grp.status.data_ptr(), ws.data_ptr())
+            ph.mark(f"merge-prep d{d}")
             _ext.check(lib.hps_merge_build(mb, s), "merge build")
+            ph.mark(f"merge d{d} x{npar} m3={m3} e={e}")
             if en0.wrap is not None:
                 _apply_wrap(solver, grp, plan.node[ids[0]], lib, s)
                 tloc[ids[0]] = (grp.wrap.pop("tw"), 0, grp.wrap["ec"])
@@ -575,7 +603,9 @@ def _build_device(solver: FactorizedSolver, order):
             for ch in tree.nodes[nid].children:
                 tloc.pop(ch, None)
     tloc.clear()
+    ph.mark("merges-done")
     _finish_checks(solver, order)
+    solver.phase_ms = ph.report()
     solver._layout = _layout(solver)
 
 
