@@ -240,59 +240,78 @@ class FactorizedSolver:
         gt = self._leaf_table(g)
         prog = self._program(1)
         lay, pool = self._layout, prog["pool"]
-        gdev = torch.as_tensor(gt, dtype=torch.float64).to(self.device, non_blocking=True).reshape(-1, 1)
-        fdev = None
+        N, P, nl = self.plan.n_gauss, self.p ** 2, self._n_leaves
+        g_rows = pool[lay["G"]:lay["G"] + nl * (self.p - 2) ** 2, 0]
+        g_rows.copy_(torch.as_tensor(gt, dtype=torch.float64).reshape(-1), non_blocking=False)
         if down:
-            fdev = torch.as_tensor(fv, dtype=torch.float64).to(self.device, non_blocking=True).reshape(-1, 1)
-        self._run(prog, fdev, gdev, down=down)
-        host = pool[:, 0].cpu().numpy()
-        N = self.plan.n_gauss
+            prog["f_in"][:, 0].copy_(torch.as_tensor(fv, dtype=torch.float64).reshape(-1))
+        self._execute(prog, down=down)
+        # D2H of the result regions only: U|W (contiguous), h_root, leaf tabulations
+        uw = pool[:2 * N, 0].cpu().numpy()
         rs = lay["hslot"][self.tree.root]
-        st = SolveState(u=host[lay["U"]:lay["U"] + N].copy(), w=host[lay["W"]:lay["W"] + N].copy(),
-                        tree=self.tree, p=self.p, q=self.q,
-                        h_root=host[rs:rs + lay["hsize"][self.tree.root]].copy())
+        st = SolveState(u=uw[:N], w=uw[N:], tree=self.tree, p=self.p, q=self.q,
+                        h_root=pool[rs:rs + lay["hsize"][self.tree.root], 0].cpu().numpy())
         gtab = gt.detach().cpu().numpy() if isinstance(gt, torch.Tensor) else np.asarray(gt)
-        st.g_tab = LeafSolutions(self._leaf_ids, range(self._n_leaves), gtab)
+        st.g_tab = LeafSolutions(self._leaf_ids, range(nl), gtab)
         if down:
-            P = self.p ** 2
-            uc = host[lay["UC"]:lay["UC"] + self._n_leaves * P].reshape(self._n_leaves, P).copy()
-            st.leaf_solutions = LeafSolutions(self._leaf_ids, range(self._n_leaves), uc)
+            uc = pool[lay["UC"]:lay["UC"] + nl * P, 0].cpu().numpy().reshape(nl, P)
+            st.leaf_solutions = LeafSolutions(self._leaf_ids, range(nl), uc)
         else:
             st.scratch = {"g": g}
         return st
 
     def solve_device(self, f: torch.Tensor, g: torch.Tensor) -> dict:
-        """Multi-RHS solve with device-resident inputs/outputs (no host round trip).
+        """Multi-RHS solve with device-resident inputs and outputs (no host round trip).
 
-        f: (nrhs, |root ext|) or (|root ext|, nrhs) handled as (rows, nrhs) after transpose;
-        g: (n_leaves, m, nrhs) interior loads in leaf-row order. Returns views into the pool:
-        u (N_gauss, nrhs), w, uc (n_leaves, P, nrhs), h_root.
+        f: (|root ext|, nrhs) Dirichlet data in plan.node[root].ext order;
+        g: (n_leaves * m, nrhs) interior loads in leaf-row order (i_ci order within a leaf).
+        Returns views into the solver's vector pool (valid until the next solve with the
+        same nrhs): u, w (N_gauss, nrhs), uc (n_leaves, P, nrhs), g.
         """
         nrhs = g.shape[-1]
         prog = self._program(nrhs)
-        self._run(prog, f.reshape(-1, nrhs), g.reshape(-1, nrhs))
         lay, pool, N = self._layout, prog["pool"], self.plan.n_gauss
-        P = self.p ** 2
+        nl, P, m = self._n_leaves, self.p ** 2, (self.p - 2) ** 2
+        pool[lay["G"]:lay["G"] + nl * m].copy_(g.reshape(-1, nrhs))
+        prog["f_in"].copy_(f.reshape(-1, nrhs))
+        self._execute(prog, down=True)
         return {"u": pool[lay["U"]:lay["U"] + N], "w": pool[lay["W"]:lay["W"] + N],
-                "uc": pool[lay["UC"]:lay["UC"] + self._n_leaves * P].view(self._n_leaves, P, nrhs),
-                "g": pool[lay["G"]:lay["G"] + self._n_leaves * (self.p - 2) ** 2]}
+                "uc": pool[lay["UC"]:lay["UC"] + nl * P].view(nl, P, nrhs),
+                "g": pool[lay["G"]:lay["G"] + nl * m]}
 
     # -- sweep program ----------------------------------------------------------------------
-    def _run(self, prog, fdev, gdev, down=True):
+    use_graphs = True
+
+    def _steps(self, prog, down=True):
+        """Enqueue one solve on the current stream: zero u/w, upward sweep, f, downward sweep."""
         lib = _ext.load()
         pool = prog["pool"]
-        lay = self._layout
         N = self.plan.n_gauss
         s = _stream_ptr()
-        pool[lay["U"]:lay["U"] + 2 * N].zero_()
-        pool[lay["G"]:lay["G"] + gdev.shape[0]].copy_(gdev)
+        pool[:2 * N].zero_()
         for step in prog["up"]:
             _ext.check(lib.hps_sweep_gemv(step, s), "upward sweep")
         if not down:
             return
-        pool.index_copy_(0, prog["root_rows"], fdev)
+        pool.index_copy_(0, prog["root_rows"], prog["f_in"])
         for step in prog["down"]:
             _ext.check(lib.hps_sweep_gemv(step, s), "downward sweep")
+
+    def _execute(self, prog, down=True):
+        if not (down and self.use_graphs):
+            self._steps(prog, down)
+            return
+        if prog.get("graph") is None:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                self._steps(prog)
+            torch.cuda.current_stream().wait_stream(side)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                self._steps(prog)
+            prog["graph"] = graph
+        prog["graph"].replay()
 
     def _program(self, nrhs):
         prog = self._sweeps.get(nrhs)
@@ -376,7 +395,9 @@ class FactorizedSolver:
                              base + grp.sc.i_ci[None, :]))
             down.append(gemv(L, c, b, _ext.mat(grp.consts["lift"], 0, b), ext, base + grp.sc.i_ce[None, :]))
         root_rows = torch.as_tensor(lay["U"] + plan.node[tree.root].ext, dtype=torch.long, device=self.device)
-        prog = {"pool": pool, "up": up, "down": down, "keep": keep, "root_rows": root_rows}
+        f_in = torch.zeros((root_rows.numel(), nrhs), dtype=torch.float64, device=self.device)
+        prog = {"pool": pool, "up": up, "down": down, "keep": keep, "root_rows": root_rows, "f_in": f_in,
+                "graph": None}
         self._sweeps[nrhs] = prog
         return prog
 
