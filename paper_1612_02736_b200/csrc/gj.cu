@@ -35,7 +35,7 @@ static int gj_panel_width(int n) {
 
 // W (batch x kb x ncols doubles) followed by the inverse column permutation (batch x n ints)
 long long gj_workspace_doubles(int batch, int n, int ncols) {
-  return (long long)batch * gj_panel_width(n) * ncols + ((long long)batch * n + 1) / 2 + 1;
+  return (long long)batch * 64 * ncols + ((long long)batch * n + 1) / 2 + 1;
 }
 
 __global__ void __launch_bounds__(GJ_THREADS) gj_panel_kernel(int n, int k0, int kb, MatB M, int* piv,
@@ -213,59 +213,106 @@ int launch_colnorm1(int batch, int n, MatB M, double* out, cudaStream_t s) {
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
+// panel width for the fused kernel: largest multiple of 4 (<= 32) whose smem fits the budget
+static int fused_kb(int n, size_t budget) {
+  int kb = n < 32 ? n : 32;
+  while (kb > 4 && gj_fused_smem(n, kb) > budget) kb -= 4;
+  return kb;
+}
+
+static int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+// Outer block width of the two-level scheme (inner: fused kernel on the NB-column block;
+// outer: row interchanges + one DMMA GEMM with K = NB over all other columns).
+constexpr int GJ_OUTER_NB = 64;
+
 int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, double* anorm,
               double* ainvnorm, int* status, cudaStream_t s) {
   if (batch <= 0 || n <= 0) return 0;
+  const int sms = sm_count();
+  const bool fused_full = n <= 256 && (batch >= sms || n <= 64);
+  if (fused_full) {
+    FusedArgs f{};
+    f.batch = batch;
+    f.n = n;
+    f.ncols = ncols;
+    f.M = M;
+    f.piv = piv;
+    f.status = status;
+    f.anorm = anorm;
+    f.ainvnorm = ainvnorm;
+    f.k_begin = 0;
+    f.k_end = n;
+    f.col_lo = 0;
+    f.col_hi = ncols;
+    f.kb = fused_kb(n, 110 * 1024);
+    f.full = 1;
+    const int grid = batch < 2 * sms ? batch : 2 * sms;
+    return launch_gj_fused(f, grid, s);
+  }
   if (anorm) {
     int rc = launch_colnorm1(batch, n, M, anorm, s);
     if (rc) return rc;
   }
-  const int kbmax = gj_panel_width(n);
-  const size_t psmem = sizeof(double) * ((size_t)n * (kbmax + 1) + 32 + 8) + sizeof(int) * 16;
-  static int configured_smem = 0;
-  if ((int)psmem > 48 * 1024 && (int)psmem > configured_smem) {
-    cudaFuncSetAttribute(gj_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-    configured_smem = (int)psmem;
-  }
-  MatB W{wbuf, (long long)kbmax * ncols, nullptr, ncols, 0};
-  for (int k0 = 0; k0 < n; k0 += kbmax) {
-    const int kb = min(kbmax, n - k0);
-    const size_t smem = sizeof(double) * ((size_t)n * (kb + 1) + 32 + 8) + sizeof(int) * 16;
-    for (int off = 0; off < batch; off += 65535) {
-      const int nb = min(65535, batch - off);
-      gj_panel_kernel<<<nb, GJ_THREADS, smem, s>>>(n, k0, kb, M, piv, status, off);
-      if (ncols > kb) {
-        dim3 g2((ncols - kb + 127) / 128, nb);
-        gj_swapcopy_kernel<<<g2, 128, 0, s>>>(n, ncols, k0, kb, M, piv, W, off);
+  const int NB = GJ_OUTER_NB;
+  MatB W{wbuf, (long long)NB * ncols, nullptr, ncols, 0};
+  for (int K0 = 0; K0 < n; K0 += NB) {
+    const int nb = min(NB, n - K0);
+    FusedArgs f{};
+    f.batch = batch;
+    f.n = n;
+    f.ncols = ncols;
+    f.M = M;
+    f.piv = piv;
+    f.status = status;
+    f.k_begin = K0;
+    f.k_end = K0 + nb;
+    f.col_lo = K0;
+    f.col_hi = K0 + nb;
+    f.kb = fused_kb(n, 200 * 1024);
+    f.full = 0;
+    int rc = launch_gj_fused(f, batch, s);
+    if (rc) return rc;
+    if (ncols > nb) {
+      for (int off = 0; off < batch; off += 65535) {
+        const int bb = min(65535, batch - off);
+        dim3 g2((ncols - nb + 127) / 128, bb);
+        gj_swapcopy_kernel<<<g2, 128, 0, s>>>(n, ncols, K0, nb, M, piv, W, off);
       }
-    }
-    if (ncols > kb) {
       GemmArgs g{};
       g.M = n;
-      g.N = ncols - kb;
-      g.K = kb;
+      g.N = ncols - nb;
+      g.K = nb;
       g.alpha = 1.0;
       g.beta = 1.0;
       g.A = M;
-      g.A.off = M.off + k0;
+      g.A.off = M.off + K0;
       g.B = W;
       g.C = M;
-      g.k0 = k0;
-      g.kb = kb;
-      int rc = launch_gemm(g, batch, MODE_GJ_UPD, s);
-      if (rc) return rc;
+      g.k0 = K0;
+      g.kb = nb;
+      if ((rc = launch_gemm(g, batch, MODE_GJ_UPD, s))) return rc;
     }
   }
   // undo the column interchanges of the inverse block (pinv lives in the workspace after W)
-  int* pinv = reinterpret_cast<int*>(wbuf + (size_t)batch * kbmax * ncols);
+  int* pinv = reinterpret_cast<int*>(wbuf + (size_t)batch * NB * ncols);
   for (int off = 0; off < batch; off += 65535) {
-    const int nb = min(65535, batch - off);
-    gj_perm_kernel<<<nb, 128, sizeof(int) * n, s>>>(n, piv, pinv, off);
+    const int bb = min(65535, batch - off);
+    gj_perm_kernel<<<bb, 128, sizeof(int) * n, s>>>(n, piv, pinv, off);
     const int rows_per_cta = 32;
     const size_t usmem = sizeof(double) * (size_t)n * 4;
     if (usmem > 48 * 1024)
       cudaFuncSetAttribute(gj_unpermute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem);
-    dim3 g3((n + rows_per_cta - 1) / rows_per_cta, nb);
+    dim3 g3((n + rows_per_cta - 1) / rows_per_cta, bb);
     gj_unpermute_kernel<<<g3, 128, usmem, s>>>(n, M, pinv, rows_per_cta, off);
   }
   if (ainvnorm) {

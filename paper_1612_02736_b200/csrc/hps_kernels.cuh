@@ -28,6 +28,22 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
 
 int launch_colnorm1(int batch, int n, MatB M, double* out, cudaStream_t s);
 
+struct FusedArgs {
+  int batch, n, ncols;
+  MatB M;
+  int* piv;            // batch x n
+  int* status;
+  double* anorm;       // full mode only
+  double* ainvnorm;
+  int k_begin, k_end;  // pivot columns processed
+  int col_lo, col_hi;  // columns updated (must contain [k_begin, k_end))
+  int kb;              // panel width
+  int ldp;             // set by the launcher
+  int full;            // 1: norms + column un-permutation
+};
+size_t gj_fused_smem(int n, int kb);
+int launch_gj_fused(const FusedArgs& a, int grid, cudaStream_t s);
+
 // Leaf-stage assembly: interior rows of the collocation matrix for each leaf.
 struct LeafAsmArgs {
   int nleaf, p;

@@ -65,7 +65,8 @@ def _gj(lib, M, n, ncols):
 
 
 @pytest.mark.parametrize("n,nrhs,batch", [(1, 0, 2), (5, 3, 4), (15, 90, 3), (33, 7, 2), (60, 240, 5),
-                                          (196, 60, 3), (300, 10, 2), (900, 124, 1)])
+                                          (196, 60, 3), (196, 60, 300), (130, 500, 150), (300, 10, 2),
+                                          (900, 124, 1), (1000, 3000, 1)])
 def test_gj_inverse_matches_numpy(lib, n, nrhs, batch):
     rng = np.random.default_rng(n)
     A = rng.standard_normal((batch, n, n)) + n ** 0.5 * np.eye(n) * rng.choice([-1, 1], size=(batch, 1, 1))

@@ -86,7 +86,7 @@ def test_config5_small_backward_euler_vs_golden():
         assert rel_maxdiff(sol, fx[f"rhs{r}_leaf_sol"]) <= 1e-10
 
 
-@pytest.mark.parametrize("n,p,q", [(2, 9, 8), (4, 12, 11), (8, 16, 15)])
+@pytest.mark.parametrize("n,p,q", [(2, 9, 8), (4, 12, 11), (8, 16, 15), (16, 16, 15)])
 def test_varcoef_vs_oracle(n, p, q):
     spec = catalog("varcoef_helmholtz", kappa=10.0)
     tree = build_uniform_tree(UNIT, n)
