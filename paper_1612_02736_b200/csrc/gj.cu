@@ -116,26 +116,51 @@ __global__ void __launch_bounds__(GJ_THREADS) gj_panel_kernel(int n, int k0, int
   }
 }
 
-// one thread per non-panel column: apply the panel's row swaps, save the pivot rows to W
+// One thread per non-panel column: apply the panel's kb row interchanges and save the kb
+// pivot rows to W. The interchanges are composed once per CTA in shared memory (rowid), so
+// each column needs only independent loads: W[j] = M[rowid[k0+j]] and, for the displaced
+// rows outside the panel (which always receive original panel rows), M[x] = M[rowid[x]].
+// Rows inside the panel are not written: the GJ update overwrites them with panel_J W.
 __global__ void gj_swapcopy_kernel(int n, int ncols, int k0, int kb, MatB M, const int* piv, MatB W,
                                    int batch_off) {
+  extern __shared__ int rowid[];  // n - k0 entries + moves
+  int* moves = rowid + (n - k0);  // [0] count, then (dst, src)
   const int item = blockIdx.y + batch_off;
+  const int* pv = piv + (long long)item * n + k0;
+  for (int x = threadIdx.x; x < n - k0; x += blockDim.x) rowid[x] = x + k0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < kb; ++j) {
+      const int p = pv[j] - k0;
+      const int t = rowid[j];
+      rowid[j] = rowid[p];
+      rowid[p] = t;
+    }
+    int nm = 0;
+    for (int j = 0; j < kb; ++j) {
+      const int x = pv[j];
+      if (x >= k0 + kb && rowid[x - k0] != x) {
+        moves[1 + 2 * nm] = x;
+        moves[2 + 2 * nm] = rowid[x - k0];
+        ++nm;
+      }
+    }
+    moves[0] = nm;
+  }
+  __syncthreads();
   const int cl = blockIdx.x * blockDim.x + threadIdx.x;
   if (cl >= ncols - kb) return;
   const int c = cl < k0 ? cl : cl + kb;
   double* Mi = M.get(item);
   const long long ld = M.ld;
-  const int* pv = piv + (long long)item * n + k0;
-  for (int j = 0; j < kb; ++j) {
-    const int r = pv[j];
-    if (r != k0 + j) {
-      const double t = Mi[(long long)r * ld + c];
-      Mi[(long long)r * ld + c] = Mi[(long long)(k0 + j) * ld + c];
-      Mi[(long long)(k0 + j) * ld + c] = t;
-    }
-  }
   double* Wi = W.get(item);
-  for (int j = 0; j < kb; ++j) Wi[(long long)j * W.ld + c] = Mi[(long long)(k0 + j) * ld + c];
+#pragma unroll 8
+  for (int j = 0; j < kb; ++j) Wi[(long long)j * W.ld + c] = Mi[(long long)rowid[j] * ld + c];
+  const int nm = moves[0];
+  for (int m = 0; m < nm; ++m) {
+    const int dst = moves[1 + 2 * m], src = moves[2 + 2 * m];
+    Mi[(long long)dst * ld + c] = Mi[(long long)src * ld + c];
+  }
 }
 
 // inverse column permutation pinv (pinv[perm[j]] = j) from the LAPACK interchange list
@@ -213,13 +238,6 @@ int launch_colnorm1(int batch, int n, MatB M, double* out, cudaStream_t s) {
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
-// panel width for the fused kernel: largest multiple of 4 (<= 32) whose smem fits the budget
-static int fused_kb(int n, size_t budget) {
-  int kb = n < 32 ? n : 32;
-  while (kb > 4 && gj_fused_smem(n, kb) > budget) kb -= 4;
-  return kb;
-}
-
 static int sm_count() {
   static int sms = 0;
   if (!sms) {
@@ -254,7 +272,6 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
     f.k_end = n;
     f.col_lo = 0;
     f.col_hi = ncols;
-    f.kb = fused_kb(n, 110 * 1024);
     f.full = 1;
     const int grid = batch < 2 * sms ? batch : 2 * sms;
     return launch_gj_fused(f, grid, s);
@@ -278,7 +295,6 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
     f.k_end = K0 + nb;
     f.col_lo = K0;
     f.col_hi = K0 + nb;
-    f.kb = fused_kb(n, 200 * 1024);
     f.full = 0;
     int rc = launch_gj_fused(f, batch, s);
     if (rc) return rc;
@@ -286,7 +302,7 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
       for (int off = 0; off < batch; off += 65535) {
         const int bb = min(65535, batch - off);
         dim3 g2((ncols - nb + 127) / 128, bb);
-        gj_swapcopy_kernel<<<g2, 128, 0, s>>>(n, ncols, K0, nb, M, piv, W, off);
+        gj_swapcopy_kernel<<<g2, 128, sizeof(int) * (n - K0 + 2 * nb + 4), s>>>(n, ncols, K0, nb, M, piv, W, off);
       }
       GemmArgs g{};
       g.M = n;

@@ -1,25 +1,27 @@
 // Fused, persistent Gauss-Jordan kernel: one CTA owns one matrix at a time and runs every
-// panel of a pivot-column range back to back (panel factorisation in shared memory, row
-// interchanges, pivot-row snapshot, DMMA trailing update), so a whole batch of small
-// inverses (leaf interior blocks at p=16: 196 x 256 augmented; low-level merges) costs one
-// launch and the matrix stays hot in L2 between panels.
+// panel of a pivot-column range back to back, so a whole batch of small inverses (leaf
+// interior blocks at p=16: 196 x 256 augmented; low tree levels) costs one launch and the
+// matrix stays hot in L2 between panels.
 //
-// Layout in shared memory (column-major panel so both the row-per-thread elimination and
-// the DMMA A-fragment loads are bank-conflict free; stride ldp = 4 mod 16 doubles):
-//   P[j*ldp + i]  panel column j, row i       (kb4 x ldp)
-//   W[j*LDW + c]  pivot row j, chunk column c (kb4 x LDW), LDW = 132 (= 4 mod 16)
-//
+// Per panel of KB columns:
+//   1. each thread holds its RPT rows of the panel in registers (row i = tid + r*256);
+//      per column: warp-shuffle argmax + one cross-warp exchange (2 __syncthreads), the
+//      pivot row and the displaced row swap through shared memory, elimination in registers;
+//   2. the factored panel goes to shared memory (column-major, stride ldp = 4 mod 16, so the
+//      DMMA A-fragment loads are bank-conflict free) and back to global;
+//   3. the KB row interchanges are composed once (rowid) so every other column needs only
+//      independent loads: W[j] = M[rowid[k0+j]] and the few displaced rows outside the panel;
+//   4. DMMA (mma.sync.m8n8k4.f64) trailing update of the other columns, in chunks of CW
+//      columns: rows in the panel get panel_J W, the rest += panel_R W.
 // Modes: full (k = 0..n over all columns, plus |A|_1, |A^-1|_1 and the final column
-// un-permutation) or sub-range (pivot columns [k_begin,k_end) updating columns
-// [col_lo,col_hi) only) — the inner level of the two-level blocking used for large n.
+// un-permutation) or sub-range (pivot columns [k_begin,k_end) updating [col_lo,col_hi)
+// only) — the inner level of the two-level blocking used for large n (gj.cu).
 #include "hps_common.cuh"
 #include "hps_kernels.cuh"
 
 namespace hps {
 
 constexpr int FU_THREADS = 256;
-constexpr int FU_CW = 128;
-constexpr int FU_LDW = FU_CW + 4;
 
 __device__ __forceinline__ double block_max_nan(double v, double* red) {
 #pragma unroll
@@ -38,24 +40,57 @@ __device__ __forceinline__ double block_max_nan(double v, double* red) {
 __device__ double colnorm_block(const double* Mi, long long ld, int n, double* red) {
   double best = 0.0;
   for (int c = threadIdx.x; c < n; c += FU_THREADS) {
-    double s = 0.0;
-    for (int r = 0; r < n; ++r) s += fabs(Mi[r * ld + c]);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int r = 0;
+    for (; r + 4 <= n; r += 4) {
+      s0 += fabs(Mi[(r + 0) * ld + c]);
+      s1 += fabs(Mi[(r + 1) * ld + c]);
+      s2 += fabs(Mi[(r + 2) * ld + c]);
+      s3 += fabs(Mi[(r + 3) * ld + c]);
+    }
+    for (; r < n; ++r) s0 += fabs(Mi[r * ld + c]);
+    const double s = (s0 + s1) + (s2 + s3);
     best = (s > best || s != s) ? s : best;
   }
   return block_max_nan(best, red);
 }
 
-__global__ void __launch_bounds__(FU_THREADS, 2) gj_fused_kernel(FusedArgs a) {
-  extern __shared__ double sm[];
-  const int n = a.n, ldp = a.ldp, kbmax4 = (a.kb + 3) & ~3;
-  double* P = sm;
-  double* W = P + (size_t)kbmax4 * ldp;
-  double* prow = W + (size_t)kbmax4 * FU_LDW;
-  double* red_v = prow + 32;
-  int* red_i = reinterpret_cast<int*>(red_v + 8);
-  int* spiv = red_i + 16;
-  int* perm = spiv + 32;
+struct FusedSmem {
+  double* P;
+  double* W;
+  double* bufA;
+  double* bufB;
+  double* red_v;
+  int* red_i;
+  int* spiv;
+  int* wsrc;
+  int* moves;  // [0] = count, then (dst, src) pairs
+  int* rowid;
+};
 
+template <int KB>
+__device__ __forceinline__ FusedSmem carve(double* sm, int n, int ldp, int ldw) {
+  constexpr int KB4 = (KB + 3) & ~3;
+  FusedSmem s;
+  s.P = sm;
+  s.W = s.P + (size_t)KB4 * ldp;
+  s.bufA = s.W + (size_t)KB4 * ldw;
+  s.bufB = s.bufA + KB4;
+  s.red_v = s.bufB + KB4;
+  s.red_i = reinterpret_cast<int*>(s.red_v + 8);
+  s.spiv = s.red_i + 8;
+  s.wsrc = s.spiv + KB4;
+  s.moves = s.wsrc + KB4;
+  s.rowid = s.moves + 2 * KB4 + 4;
+  return s;
+}
+
+template <int KB, int RPT>
+__global__ void __launch_bounds__(FU_THREADS, (RPT >= 8 ? 1 : 2)) gj_fused_kernel(FusedArgs a) {
+  constexpr int KB4 = (KB + 3) & ~3;
+  extern __shared__ double sm[];
+  const int n = a.n, ldp = a.ldp, ldw = a.ldw, CW = a.cw;
+  FusedSmem S = carve<KB>(sm, n, ldp, ldw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
 
@@ -65,28 +100,35 @@ __global__ void __launch_bounds__(FU_THREADS, 2) gj_fused_kernel(FusedArgs a) {
     int* piv = a.piv + (long long)item * n;
     int flag = 0;
     if (a.full && a.anorm) {
-      const double v = colnorm_block(Mi, ld, n, red_v);
+      const double v = colnorm_block(Mi, ld, n, S.red_v);
       if (tid == 0) a.anorm[item] = v;
     }
-    for (int k0 = a.k_begin; k0 < a.k_end; k0 += a.kb) {
-      const int kb = min(a.kb, a.k_end - k0);
-      const int kb4 = (kb + 3) & ~3;
-      __syncthreads();
-      for (int e = tid; e < n * kb; e += FU_THREADS) {
-        const int i = e / kb, j = e - i * kb;
-        P[j * ldp + i] = Mi[i * ld + k0 + j];
-      }
-      for (int e = tid; e < (kb4 - kb) * ldp; e += FU_THREADS) P[kb * ldp + e] = 0.0;
-      __syncthreads();
+    for (int k0 = a.k_begin; k0 < a.k_end; k0 += KB) {
+      const int kbc = min(KB, a.k_end - k0);
+      __syncthreads();  // previous panel's smem (P, W, rowid) fully consumed
 
-      // ---- panel factorisation (pivot rows searched from k0+j, ties -> smallest index)
-      for (int j = 0; j < kb; ++j) {
+      // ---- 1. panel rows -> registers
+      double row[RPT][KB];
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int i = tid + r * FU_THREADS;
+        const double* src = Mi + (long long)(i < n ? i : 0) * ld + k0;
+#pragma unroll
+        for (int t = 0; t < KB; ++t) row[r][t] = (i < n && t < kbc) ? src[t] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        if (j >= kbc) break;
         const int cj = k0 + j;
         double best = -1.0;
         int bi = n;
-        for (int i = cj + tid; i < n; i += FU_THREADS) {
-          const double v = fabs(P[j * ldp + i]);
-          if (v > best) { best = v; bi = i; }
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          const int i = tid + r * FU_THREADS;
+          if (i < n && i >= cj) {
+            const double v = fabs(row[r][j]);
+            if (v > best) { best = v; bi = i; }
+          }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -94,69 +136,110 @@ __global__ void __launch_bounds__(FU_THREADS, 2) gj_fused_kernel(FusedArgs a) {
           const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
           if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
         }
-        if (lane == 0) { red_v[warp] = best; red_i[warp] = bi; }
+        if (lane == 0) { S.red_v[warp] = best; S.red_i[warp] = bi; }
         __syncthreads();
+        double b = S.red_v[0];
+        int pr = S.red_i[0];
+#pragma unroll
+        for (int w = 1; w < FU_THREADS / 32; ++w) {
+          const double vw = S.red_v[w];
+          const int iw = S.red_i[w];
+          if (vw > b || (vw == b && iw < pr)) { b = vw; pr = iw; }
+        }
+        if (pr >= n) pr = cj;
         if (tid == 0) {
-          double b = red_v[0];
-          int bix = red_i[0];
-          for (int w = 1; w < FU_THREADS / 32; ++w)
-            if (red_v[w] > b || (red_v[w] == b && red_i[w] < bix)) { b = red_v[w]; bix = red_i[w]; }
-          if (bix >= n) bix = cj;
           if (!(b > 0.0)) flag = 1;
-          red_i[8] = bix;
-          spiv[j] = bix;
-          piv[cj] = bix;
+          S.spiv[j] = pr;
+          piv[cj] = pr;
         }
-        __syncthreads();
-        const int pr = red_i[8];
-        if (pr != cj && tid < kb) {
-          const double t = P[tid * ldp + pr];
-          P[tid * ldp + pr] = P[tid * ldp + cj];
-          P[tid * ldp + cj] = t;
-        }
-        __syncthreads();
-        if (tid < kb) {
-          const double inv = 1.0 / P[j * ldp + cj];
-          prow[tid] = (tid == j) ? inv : P[tid * ldp + cj] * inv;
-        }
-        __syncthreads();
-        for (int i = tid; i < n; i += FU_THREADS) {
-          if (i == cj) {
-            for (int t = 0; t < kb; ++t) P[t * ldp + i] = prow[t];
-          } else {
-            const double f = P[j * ldp + i];
-            P[j * ldp + i] = 0.0;
-            for (int t = 0; t < kb; ++t) P[t * ldp + i] -= f * prow[t];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          const int i = tid + r * FU_THREADS;
+          if (i == pr) {
+#pragma unroll
+            for (int t = 0; t < KB; ++t) S.bufA[t] = row[r][t];
+          }
+          if (i == cj && pr != cj) {
+#pragma unroll
+            for (int t = 0; t < KB; ++t) S.bufB[t] = row[r][t];
           }
         }
         __syncthreads();
-      }
-      for (int e = tid; e < n * kb; e += FU_THREADS) {
-        const int i = e / kb, j = e - i * kb;
-        Mi[i * ld + k0 + j] = P[j * ldp + i];
+        const double inv = 1.0 / S.bufA[j];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          const int i = tid + r * FU_THREADS;
+          if (i == pr && pr != cj) {
+#pragma unroll
+            for (int t = 0; t < KB; ++t) row[r][t] = S.bufB[t];
+          }
+          if (i == cj) {
+#pragma unroll
+            for (int t = 0; t < KB; ++t) row[r][t] = (t == j) ? inv : S.bufA[t] * inv;
+          } else {
+            const double f = row[r][j];
+#pragma unroll
+            for (int t = 0; t < KB; ++t) row[r][t] = ((t == j) ? 0.0 : row[r][t]) - f * ((t == j) ? inv : S.bufA[t] * inv);
+          }
+        }
       }
 
-      // ---- trailing update of the other columns of [col_lo, col_hi), in chunks of FU_CW
-      const int nlog = (a.col_hi - a.col_lo) - kb;
-      for (int c0 = 0; c0 < nlog; c0 += FU_CW) {
-        const int cw = min(FU_CW, nlog - c0);
-        __syncthreads();
-        for (int cc = tid; cc < FU_CW; cc += FU_THREADS) {
+      // ---- 2. factored panel -> shared (column-major) and global; composed interchanges
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int i = tid + r * FU_THREADS;
+        if (i < n) {
+          double* dst = Mi + (long long)i * ld + k0;
+#pragma unroll
+          for (int t = 0; t < KB; ++t) {
+            if (t < kbc) dst[t] = row[r][t];
+            S.P[t * ldp + i] = (t < kbc) ? row[r][t] : 0.0;
+          }
+        }
+      }
+      for (int e = tid; e < (KB4 - KB) * ldp; e += FU_THREADS) S.P[KB * ldp + e] = 0.0;
+      for (int x = k0 + tid; x < n; x += FU_THREADS) S.rowid[x] = x;
+      __syncthreads();
+      if (tid == 0) {
+        for (int j = 0; j < kbc; ++j) {
+          const int p = S.spiv[j];
+          const int t = S.rowid[k0 + j];
+          S.rowid[k0 + j] = S.rowid[p];
+          S.rowid[p] = t;
+        }
+        int nm = 0;
+        for (int j = 0; j < kbc; ++j) {
+          S.wsrc[j] = S.rowid[k0 + j];
+          const int x = S.spiv[j];
+          if (x >= k0 + kbc && S.rowid[x] != x) {
+            S.moves[1 + 2 * nm] = x;
+            S.moves[2 + 2 * nm] = S.rowid[x];
+            ++nm;
+          }
+        }
+        S.moves[0] = nm;
+      }
+      __syncthreads();
+
+      // ---- 3./4. other columns of [col_lo, col_hi), chunks of CW
+      const int nlog = (a.col_hi - a.col_lo) - kbc;
+      const int nm = S.moves[0];
+      for (int c0 = 0; c0 < nlog; c0 += CW) {
+        const int cw = min(CW, nlog - c0);
+        if (c0 > 0) __syncthreads();
+        for (int cc = tid; cc < ldw; cc += FU_THREADS) {
           if (cc < cw) {
             int pc = a.col_lo + c0 + cc;
-            if (pc >= k0) pc += kb;
-            for (int j = 0; j < kb; ++j) {
-              const int r = spiv[j];
-              if (r != k0 + j) {
-                const double t = Mi[r * ld + pc];
-                Mi[r * ld + pc] = Mi[(k0 + j) * ld + pc];
-                Mi[(k0 + j) * ld + pc] = t;
-              }
+            if (pc >= k0) pc += kbc;
+#pragma unroll 8
+            for (int j = 0; j < KB4; ++j) S.W[j * ldw + cc] = (j < kbc) ? Mi[(long long)S.wsrc[j] * ld + pc] : 0.0;
+            for (int mv = 0; mv < nm; ++mv) {
+              const int dst = S.moves[1 + 2 * mv], src = S.moves[2 + 2 * mv];
+              Mi[(long long)dst * ld + pc] = Mi[(long long)src * ld + pc];
             }
-            for (int j = 0; j < kb; ++j) W[j * FU_LDW + cc] = Mi[(k0 + j) * ld + pc];
-            for (int j = kb; j < kb4; ++j) W[j * FU_LDW + cc] = 0.0;
           } else {
-            for (int j = 0; j < kb4; ++j) W[j * FU_LDW + cc] = 0.0;
+#pragma unroll
+            for (int j = 0; j < KB4; ++j) S.W[j * ldw + cc] = 0.0;
           }
         }
         __syncthreads();
@@ -171,25 +254,27 @@ __global__ void __launch_bounds__(FU_THREADS, 2) gj_fused_kernel(FusedArgs a) {
             for (int h = 0; h < 2; ++h) {
               const int cl = cc0 + jj * 8 + tq * 2 + h;
               int pc = a.col_lo + c0 + cl;
-              if (pc >= k0) pc += kb;
+              if (pc >= k0) pc += kbc;
               pcol[jj][h] = (cl < cw) ? pc : -1;
             }
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int r = r0 + i * 8 + gq;
-            const bool live = r < n && !(r >= k0 && r < k0 + kb);
+            const bool live = r < n && !(r >= k0 && r < k0 + kbc);
+            const double* crow = Mi + (long long)(r < n ? r : 0) * ld;
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj)
 #pragma unroll
               for (int h = 0; h < 2; ++h)
-                acc[i][jj][h] = (live && pcol[jj][h] >= 0) ? Mi[r * ld + pcol[jj][h]] : 0.0;
+                acc[i][jj][h] = (live && pcol[jj][h] >= 0) ? crow[pcol[jj][h]] : 0.0;
           }
-          for (int k = 0; k < kb4; k += 4) {
+#pragma unroll
+          for (int k = 0; k < KB4; k += 4) {
             double af[4], bf[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) af[i] = P[(k + tq) * ldp + r0 + i * 8 + gq];
+            for (int i = 0; i < 4; ++i) af[i] = S.P[(k + tq) * ldp + r0 + i * 8 + gq];
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) bf[jj] = W[(k + tq) * FU_LDW + cc0 + jj * 8 + gq];
+            for (int jj = 0; jj < 4; ++jj) bf[jj] = S.W[(k + tq) * ldw + cc0 + jj * 8 + gq];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -199,11 +284,12 @@ __global__ void __launch_bounds__(FU_THREADS, 2) gj_fused_kernel(FusedArgs a) {
           for (int i = 0; i < 4; ++i) {
             const int r = r0 + i * 8 + gq;
             if (r >= n) continue;
+            double* crow = Mi + (long long)r * ld;
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj)
 #pragma unroll
               for (int h = 0; h < 2; ++h)
-                if (pcol[jj][h] >= 0) Mi[r * ld + pcol[jj][h]] = acc[i][jj][h];
+                if (pcol[jj][h] >= 0) crow[pcol[jj][h]] = acc[i][jj][h];
           }
         }
       }
@@ -213,6 +299,7 @@ __global__ void __launch_bounds__(FU_THREADS, 2) gj_fused_kernel(FusedArgs a) {
 
     if (a.full) {
       // undo the column interchanges of the inverse: inv[:, perm[j]] = M[:, j]
+      int* perm = S.rowid;
       for (int j = tid; j < n; j += FU_THREADS) perm[j] = j;
       __syncthreads();
       if (tid == 0) {
@@ -224,43 +311,71 @@ __global__ void __launch_bounds__(FU_THREADS, 2) gj_fused_kernel(FusedArgs a) {
         }
       }
       __syncthreads();
-      double* buf = P + (size_t)warp * n;
+      double* buf = S.P + (size_t)warp * n;
       for (int r = warp; r < n; r += FU_THREADS / 32) {
-        double* row = Mi + r * ld;
-        for (int c = lane; c < n; c += 32) buf[c] = row[c];
+        double* rowp = Mi + (long long)r * ld;
+#pragma unroll 8
+        for (int c = lane; c < n; c += 32) buf[c] = rowp[c];
         __syncwarp();
-        for (int c = lane; c < n; c += 32) row[perm[c]] = buf[c];
+#pragma unroll 8
+        for (int c = lane; c < n; c += 32) rowp[perm[c]] = buf[c];
         __syncwarp();
       }
       __syncthreads();
       if (a.ainvnorm) {
-        const double v = colnorm_block(Mi, ld, n, red_v);
+        const double v = colnorm_block(Mi, ld, n, S.red_v);
         if (tid == 0) a.ainvnorm[item] = v;
       }
     }
   }
 }
 
-size_t gj_fused_smem(int n, int kb) {
-  const int kb4 = (kb + 3) & ~3;
-  const int ldp = ((n + 15) & ~15) + 4;
-  return sizeof(double) * ((size_t)kb4 * ldp + (size_t)kb4 * FU_LDW + 32 + 8) + sizeof(int) * (16 + 32 + n + 8);
+static int round_ldp(int n) { return ((n + 15) & ~15) + 4; }
+
+template <int KB>
+static size_t fused_smem_bytes(int n, int ldw) {
+  constexpr int KB4 = (KB + 3) & ~3;
+  return sizeof(double) * ((size_t)KB4 * round_ldp(n) + (size_t)KB4 * ldw + 2 * KB4 + 8) +
+         sizeof(int) * (8 + 2 * KB4 + 2 * KB4 + 4 + (size_t)n + 4);
 }
 
-int gj_fused_ldp(int n) { return ((n + 15) & ~15) + 4; }
-
-int launch_gj_fused(const FusedArgs& a0, int grid, cudaStream_t s) {
-  FusedArgs a = a0;
-  a.ldp = gj_fused_ldp(a.n);
-  const size_t smem = gj_fused_smem(a.n, a.kb);
-  if (smem > 227 * 1024) return 1;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaFuncSetAttribute(gj_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    configured = 227 * 1024;
+template <int KB, int RPT>
+static int launch_variant(FusedArgs a, int grid, cudaStream_t s) {
+  a.ldp = round_ldp(a.n);
+  // chunk width: all other columns at once when they fit the budget, else 128
+  const int others = (a.col_hi - a.col_lo) - 1;
+  int cw = others < 256 ? others : 256;
+  size_t smem = 0;
+  for (;;) {
+    const int ldw = ((cw + 15) & ~15) + 4;
+    smem = fused_smem_bytes<KB>(a.n, ldw);
+    if (smem <= 110 * 1024 || cw <= 32) {
+      a.cw = cw;
+      a.ldw = ldw;
+      break;
+    }
+    cw -= 32;
   }
-  gj_fused_kernel<<<grid, FU_THREADS, smem, s>>>(a);
+  if (smem > 227 * 1024) return 1;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(gj_fused_kernel<KB, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  gj_fused_kernel<KB, RPT><<<grid, FU_THREADS, smem, s>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
+int gj_fused_panel_width(int n, int full) {
+  if (full && n <= 256) return 28;
+  if (n <= 512) return 16;
+  return 8;
+}
+
+int launch_gj_fused(const FusedArgs& a, int grid, cudaStream_t s) {
+  const int kb = gj_fused_panel_width(a.n, a.full);
+  if (a.n <= 256 && kb == 28) return launch_variant<28, 1>(a, grid, s);
+  if (a.n <= 512) return launch_variant<16, 2>(a, grid, s);
+  if (a.n <= 1024) return launch_variant<8, 4>(a, grid, s);
+  if (a.n <= 2048) return launch_variant<8, 8>(a, grid, s);
+  return 1;
 }
 
 }  // namespace hps

@@ -37,11 +37,10 @@ struct FusedArgs {
   double* ainvnorm;
   int k_begin, k_end;  // pivot columns processed
   int col_lo, col_hi;  // columns updated (must contain [k_begin, k_end))
-  int kb;              // panel width
-  int ldp;             // set by the launcher
   int full;            // 1: norms + column un-permutation
+  int ldp, ldw, cw;    // set by the launcher
 };
-size_t gj_fused_smem(int n, int kb);
+int gj_fused_panel_width(int n, int full);
 int launch_gj_fused(const FusedArgs& a, int grid, cudaStream_t s);
 
 // Leaf-stage assembly: interior rows of the collocation matrix for each leaf.
