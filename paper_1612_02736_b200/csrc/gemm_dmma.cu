@@ -123,8 +123,234 @@ __global__ void __launch_bounds__(128) gemm_dmma_kernel(GemmArgs g, int batch_of
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Large-tile variant for the big contractions (GJ trailing updates with K = 64, merge
+// T_new = T_ei S, wraps): CTA tile 128x128, BK 16, 8 warps (2 x 4), warp tile 64x32
+// (8 x 4 DMMA blocks, 64 f64 accumulators / thread), 3-stage cp.async pipeline with 16-byte
+// copies when every operand is 16-byte aligned (else 8-byte copies). Fragment loads use the
+// same conflict-free paddings (A row stride 20, B row stride 132 doubles).
+constexpr int BB_M = 128, BB_K = 16, BB_STAGES = 3;
+constexpr int BA_LD = BB_K + 4;
+constexpr int BA_STAGE = BB_M * BA_LD;
+template <int BN> struct BigCfg {
+  static constexpr int THREADS = BN * 2;          // warps = BN / 16, warp tile 64 x 32
+  static constexpr int BS_LD = BN + 4;            // = 4 mod 16 doubles
+  static constexpr int B_STAGE = BB_K * BS_LD;
+  static constexpr int MINB = BN == 128 ? 1 : 2;  // 128x64 tiles: two CTAs per SM overlap
+  static constexpr size_t SMEM = sizeof(double) * BB_STAGES * (BA_STAGE + B_STAGE);
+};
+
+__device__ __forceinline__ void cp_async16_part(void* smem, const void* gmem, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes));
+}
+
+template <int MODE, bool VEC, int BN>
+__global__ void __launch_bounds__(BigCfg<BN>::THREADS, BigCfg<BN>::MINB) gemm_big_kernel(GemmArgs g, int batch_off) {
+  using Cfg = BigCfg<BN>;
+  constexpr int NT = Cfg::THREADS;
+  constexpr int WN = BN / 32;  // warps along n
+  extern __shared__ __align__(16) double gsm[];
+  double* As = gsm;
+  double* Bs = gsm + BB_STAGES * BA_STAGE;
+  const int item = blockIdx.z + batch_off;
+  const int m0 = blockIdx.y * BB_M, n0 = blockIdx.x * BN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp / WN) * 64, wn = (warp % WN) * 32;
+  const int gq = lane >> 2, tq = lane & 3;
+  const double* A = g.A.get(item);
+  const double* B = g.B.get(item);
+  double* C = g.C.get(item);
+  const long long lda = g.A.ld, ldb = g.B.ld, ldc = g.C.ld;
+  const int M = g.M, N = g.N, K = g.K;
+  auto colmap = [&](int c) { return (MODE == MODE_GJ_UPD && c >= g.k0) ? c + g.kb : c; };
+
+  auto load_tile = [&](int stage, int k) {
+    double* as = As + stage * BA_STAGE;
+    double* bs = Bs + stage * Cfg::B_STAGE;
+    if (VEC) {
+#pragma unroll
+      for (int it = 0; it < (BB_M * BB_K / 2) / NT; ++it) {
+        const int idx = tid + it * NT;
+        const int mm = idx >> 3, kk = (idx & 7) * 2;
+        const int r = m0 + mm, kc = k + kk;
+        const int bytes = (r < M) ? min(16, max(0, (K - kc) * 8)) : 0;
+        cp_async16_part(as + mm * BA_LD + kk, bytes ? (A + r * lda + kc) : A, bytes);
+      }
+#pragma unroll
+      for (int it = 0; it < (BB_K * BN / 2) / NT; ++it) {
+        const int idx = tid + it * NT;
+        const int kk = idx / (BN / 2), nn = (idx % (BN / 2)) * 2;
+        const int c = n0 + nn, kr = k + kk;
+        const int bytes = (kr < K) ? min(16, max(0, (N - c) * 8)) : 0;
+        cp_async16_part(bs + kk * Cfg::BS_LD + nn, bytes ? (B + kr * ldb + colmap(c)) : B, bytes);
+      }
+    } else {
+#pragma unroll
+      for (int it = 0; it < (BB_M * BB_K) / NT; ++it) {
+        const int idx = tid + it * NT;
+        const int mm = idx >> 4, kk = idx & 15;
+        const int r = m0 + mm, kc = k + kk;
+        const bool ok = r < M && kc < K;
+        cp_async8(as + mm * BA_LD + kk, ok ? (A + r * lda + kc) : A, ok);
+      }
+#pragma unroll
+      for (int it = 0; it < (BB_K * BN) / NT; ++it) {
+        const int idx = tid + it * NT;
+        const int kk = idx / BN, nn = idx % BN;
+        const int c = n0 + nn, kr = k + kk;
+        const bool ok = c < N && kr < K;
+        cp_async8(bs + kk * Cfg::BS_LD + nn, ok ? (B + kr * ldb + colmap(c)) : B, ok);
+      }
+    }
+  };
+
+  const int ktiles = (K + BB_K - 1) / BB_K;
+#pragma unroll
+  for (int st = 0; st < BB_STAGES - 1; ++st) {
+    if (st < ktiles) load_tile(st, st * BB_K);
+    cp_async_commit();
+  }
+
+  // alpha == 1: accumulators start from C (rows outside the GJ panel / beta != 0), loaded
+  // straight into the accumulator registers so all C reads are in flight together while the
+  // pipeline fills; beta and the bias are applied in registers afterwards.
+  const bool preload = (g.alpha == 1.0);
+  double acc[8][4][2];
+  int pcol[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) pcol[j] = colmap(n0 + wn + j * 8 + tq * 2);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = m0 + wm + i * 8 + gq;
+    const bool rowload = preload && r < M && (MODE == MODE_GJ_UPD ? !(r >= g.k0 && r < g.k0 + g.kb) : g.beta != 0.0);
+    const double* crow = C + (long long)(r < M ? r : 0) * ldc;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = n0 + wn + j * 8 + tq * 2;
+      if (VEC) {
+        double2 o = make_double2(0.0, 0.0);
+        if (rowload && c + 1 < N) o = *reinterpret_cast<const double2*>(crow + pcol[j]);
+        else if (rowload && c < N) o.x = crow[pcol[j]];
+        acc[i][j][0] = o.x;
+        acc[i][j][1] = o.y;
+      } else {
+        acc[i][j][0] = (rowload && c < N) ? crow[colmap(c)] : 0.0;
+        acc[i][j][1] = (rowload && c + 1 < N) ? crow[colmap(c + 1)] : 0.0;
+      }
+    }
+  }
+  if (preload && MODE == MODE_GEMM && (g.beta != 1.0 || g.bias)) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = m0 + wm + i * 8 + gq;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = n0 + wn + j * 8 + tq * 2 + h;
+          double v = acc[i][j][h] * g.beta;
+          if (g.bias && r < M && c < N) v += g.bias[(long long)r * g.ldbias + c];
+          acc[i][j][h] = v;
+        }
+    }
+  }
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_async_wait<BB_STAGES - 2>();
+    __syncthreads();
+    const int nxt = kt + BB_STAGES - 1;
+    if (nxt < ktiles) load_tile(nxt % BB_STAGES, nxt * BB_K);
+    cp_async_commit();
+    const double* as = As + (kt % BB_STAGES) * BA_STAGE;
+    const double* bs = Bs + (kt % BB_STAGES) * Cfg::B_STAGE;
+#pragma unroll
+    for (int k4 = 0; k4 < BB_K; k4 += 4) {
+      double af[8], bf[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) af[i] = as[(wm + i * 8 + gq) * BA_LD + k4 + tq];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = bs[(k4 + tq) * Cfg::BS_LD + wn + j * 8 + gq];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = m0 + wm + i * 8 + gq;
+    if (r >= M) continue;
+    double beta = g.beta;
+    if (MODE == MODE_GJ_UPD) beta = (r >= g.k0 && r < g.k0 + g.kb) ? 0.0 : 1.0;
+    double* crow = C + r * ldc;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = n0 + wn + j * 8 + tq * 2;
+      if (preload) {
+        if (VEC && c + 1 < N) {
+          *reinterpret_cast<double2*>(crow + pcol[j]) = make_double2(acc[i][j][0], acc[i][j][1]);
+        } else {
+          if (c < N) crow[colmap(c)] = acc[i][j][0];
+          if (c + 1 < N) crow[colmap(c + 1)] = acc[i][j][1];
+        }
+        continue;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (c + h < N) {
+          const int pc = colmap(c + h);
+          double v = g.alpha * acc[i][j][h];
+          if (beta != 0.0) v += beta * crow[pc];
+          if (MODE == MODE_GEMM && g.bias) v += g.bias[(long long)r * g.ldbias + c + h];
+          crow[pc] = v;
+        }
+      }
+    }
+  }
+}
+
+static bool aligned16(const MatB& m) {
+  if (m.ptrs) return false;
+  const uintptr_t p = reinterpret_cast<uintptr_t>(m.base + m.off);
+  return (p % 16 == 0) && (m.ld % 2 == 0) && (m.stride % 2 == 0);
+}
+
+template <int MODE, int BN>
+static void launch_big(const GemmArgs& g, int batch, cudaStream_t s) {
+  using Cfg = BigCfg<BN>;
+  const bool vec = aligned16(g.A) && aligned16(g.B) && aligned16(g.C) &&
+                   (MODE != MODE_GJ_UPD || (g.k0 % 2 == 0 && g.kb % 2 == 0));
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(gemm_big_kernel<MODE, true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    cudaFuncSetAttribute(gemm_big_kernel<MODE, false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    configured = true;
+  }
+  const int gx = (g.N + BN - 1) / BN, gy = (g.M + BB_M - 1) / BB_M;
+  for (int off = 0; off < batch; off += 65535) {
+    dim3 grid(gx, gy, min(65535, batch - off));
+    if (vec)
+      gemm_big_kernel<MODE, true, BN><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(g, off);
+    else
+      gemm_big_kernel<MODE, false, BN><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(g, off);
+  }
+}
+
 int launch_gemm(const GemmArgs& g, int batch, int mode, cudaStream_t s) {
   if (batch <= 0 || g.M <= 0 || g.N <= 0) return 0;
+  if (g.M >= 96 && g.N >= 64 && g.K >= 16) {
+    // read-modify-write updates with short K are memory-heavy: 128x64 tiles, 2 CTAs/SM
+    const bool rmw = mode == MODE_GJ_UPD || g.beta != 0.0;
+    if (mode == MODE_GEMM) {
+      if (rmw || g.N < 96) launch_big<MODE_GEMM, 64>(g, batch, s);
+      else launch_big<MODE_GEMM, 128>(g, batch, s);
+    } else {
+      launch_big<MODE_GJ_UPD, 64>(g, batch, s);
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : 2;
+  }
   dim3 block(128);
   const int gx = (g.N + GB_N - 1) / GB_N, gy = (g.M + GB_M - 1) / GB_M;
   for (int off = 0; off < batch; off += 65535) {

@@ -280,7 +280,9 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
     int rc = launch_colnorm1(batch, n, M, anorm, s);
     if (rc) return rc;
   }
-  const int NB = GJ_OUTER_NB;
+  // equal outer blocks (multiple of 4, <= 64) so no narrow tail update is left over
+  const int nblk = (n + GJ_OUTER_NB - 1) / GJ_OUTER_NB;
+  const int NB = (((n + nblk - 1) / nblk) + 3) & ~3;
   MatB W{wbuf, (long long)NB * ncols, nullptr, ncols, 0};
   for (int K0 = 0; K0 < n; K0 += NB) {
     const int nb = min(NB, n - K0);

@@ -20,7 +20,8 @@ def _stream():
 
 
 @pytest.mark.parametrize("M,N,K,batch", [(1, 1, 1, 1), (64, 64, 16, 3), (65, 70, 33, 5), (196, 60, 60, 7),
-                                         (60, 196, 196, 2), (300, 129, 77, 1)])
+                                         (60, 196, 196, 2), (300, 129, 77, 1), (256, 256, 64, 3),
+                                         (257, 131, 33, 2), (130, 250, 48, 1), (1000, 700, 200, 1)])
 def test_gemm_batched(lib, M, N, K, batch):
     g = torch.Generator(device="cuda").manual_seed(M * 1000 + N)
     A = torch.randn(batch, M, K, dtype=torch.float64, device="cuda", generator=g)
