@@ -368,6 +368,14 @@ def run_ours(args, rank, ws):
                "sample": f"{sdesc}: oracle build ({tb:.1f} s) + best of 3 solves ({ts * 1e3:.1f} ms), "
                          f"OPENBLAS threads={th}"}
 
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh).get(f"config{args.config}:leaf_down_gemv_nrhs{nrhs}")
+        if tr and args.n in (0, 64):
+            traffic = tr["dram_bytes_read"] + tr["dram_bytes_write"]
+    except Exception:
+        traffic = None
     sb_ops, sb_vec = solve_bytes(tree, plan, p, q, nrhs)
     line = {
         "metric": "HPS solve Mpts/s per RHS", "value": round(value, 3), "unit": "Mpts/s per RHS",
@@ -378,7 +386,8 @@ def run_ours(args, rank, ws):
                    "l2": "operators (%.2f GB) exceed the 126 MB L2; no flush needed" % (sb_ops / 1e9),
                    "parallelism": f"replicas over RHS x{ws}" if ws > 1 else "1 GPU"},
         "roofline": {"bound": "hbm", "kernel": "gemv_gather (leaf downward sweep)", "achieved": round(achieved, 1),
-                     "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                     "algorithmic_bytes": kbytes,
                      "peak_source": hbm_src},
         "solve_roofline": {"bytes_per_step": sb_ops + sb_vec, "achieved_gbs": round((sb_ops + sb_vec) / per / 1e9, 1),
                            "frac": round((sb_ops + sb_vec) / per / 1e9 / hbm_peak, 4)},
