@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define HPS_ABI_VERSION 1
+#define HPS_ABI_VERSION 2
 
 enum hps_status { HPS_OK = 0, HPS_EINVAL = 1, HPS_ECUDA = 2 };
 
@@ -122,7 +122,10 @@ int hps_merge_build(const hps_merge_batch* b, void* stream);
 
 /* One batched gather-GEMV of the solve sweeps. pool: rows x nrhs vector arena (RHS fastest).
  *   x_i[k][j] = pool[xidx[i][k]][j] - (x2idx ? pool[x2idx[i][k]][j] : 0)
- *   pool[oidx[i][r]][j] = sum_k A_i[r][k] x_i[k][j] + (aidx ? pool[aidx[i][r]][j] : 0)
+ *   y1 = pool[oidx[i][r]][j] = sum_k A_i[r][k] x_i[k][j] + (aidx ? pool[aidx[i][r]][j] : 0)
+ * Optional fused second stage (mode2), same launch:
+ *   mode2 = 1 (tail):  pool[o2idx[i][r]] = A2_i x_i[K-K2 .. K)          (leaf down, exterior rows)
+ *   mode2 = 2 (chain): pool[o2idx[i][r]] = A2_i y1 + pool[a2idx[i][r]]  (parent up: w3 -> h)
  * Output rows must not alias input rows within one call. nrhs <= 16. */
 typedef struct {
   int nitems, R, K, nrhs;
@@ -132,6 +135,10 @@ typedef struct {
   const int* x2idx;
   const int* aidx;
   const int* oidx;
+  int mode2, R2, K2;
+  hps_mat_batch A2;
+  const int* a2idx;
+  const int* o2idx;
 } hps_gemv_batch;
 int hps_sweep_gemv(const hps_gemv_batch* g, void* stream);
 

@@ -41,13 +41,16 @@ class MergeBatch(C.Structure):
 class GemvBatch(C.Structure):
     _fields_ = [("nitems", C.c_int), ("R", C.c_int), ("K", C.c_int), ("nrhs", C.c_int),
                 ("A", MatBatch), ("pool", C.c_void_p), ("xidx", C.c_void_p),
-                ("x2idx", C.c_void_p), ("aidx", C.c_void_p), ("oidx", C.c_void_p)]
+                ("x2idx", C.c_void_p), ("aidx", C.c_void_p), ("oidx", C.c_void_p),
+                ("mode2", C.c_int), ("R2", C.c_int), ("K2", C.c_int), ("A2", MatBatch),
+                ("a2idx", C.c_void_p), ("o2idx", C.c_void_p)]
 
 
 EXPORTS = ("hps_abi_version", "hps_status_string", "hps_gemm_batched", "hps_gj_workspace_bytes",
            "hps_gj_invert_batched", "hps_leaf_workspace_bytes", "hps_leaf_build",
            "hps_merge_workspace_bytes", "hps_merge_build", "hps_sweep_gemv")
 
+ABI_VERSION = 2
 _lib = None
 _lock = threading.Lock()
 
@@ -92,7 +95,7 @@ def load(build_if_missing: bool = True):
         lib.hps_sweep_gemv.argtypes = [C.POINTER(GemvBatch), C.c_void_p]
         for name in EXPORTS:
             getattr(lib, name)
-        if lib.hps_abi_version() != 1:
+        if lib.hps_abi_version() != ABI_VERSION:
             raise ExtensionError("HPS extension ABI version mismatch")
         _lib = lib
         return lib

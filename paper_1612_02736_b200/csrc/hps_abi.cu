@@ -192,6 +192,17 @@ int hps_sweep_gemv(const hps_gemv_batch* gb, void* stream) {
   a.x2idx = gb->x2idx;
   a.aidx = gb->aidx;
   a.oidx = gb->oidx;
+  a.mode2 = gb->mode2;
+  a.R2 = gb->R2;
+  a.K2 = gb->K2;
+  a.A2 = to_matb(&gb->A2);
+  a.a2idx = gb->a2idx;
+  a.o2idx = gb->o2idx;
+  a.xstride = a.K;
+  a.ostride = a.R;
+  if (a.mode2 && (!a.o2idx || a.R2 <= 0 || a.K2 <= 0 || (a.mode2 == 1 && a.K2 > a.K) ||
+                  (a.mode2 == 2 && a.K2 != a.R) || a.mode2 > 2))
+    return HPS_EINVAL;
   return launch_gemv_gather(a, (cudaStream_t)stream);
 }
 

@@ -82,6 +82,14 @@ struct GemvArgs {
   const int* x2idx;  // [nitems][K] or null
   const int* aidx;   // [nitems][R] or null
   const int* oidx;   // [nitems][R]
+  // optional second stage: 1 = tail  y2 = A2 x[K-K2:K)   (leaf down: exterior rows = L u_ge)
+  //                        2 = chain y2 = A2 y1 + add2   (parent up: h = T_ei w3 + [h_a; h_b])
+  int mode2, R2, K2;
+  MatB A2;
+  const int* a2idx;  // [nitems][R2] or null
+  const int* o2idx;  // [nitems][R2]
+  long long xstride; // per-item stride of xidx/x2idx (default K) and of aidx/oidx (default R)
+  long long ostride;
 };
 int launch_gemv_gather(const GemvArgs& a, cudaStream_t s);
 

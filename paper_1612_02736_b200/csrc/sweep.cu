@@ -29,8 +29,8 @@ __global__ void __launch_bounds__(SW_THREADS) gemv_gather_kernel(GemvArgs a, int
   const int r1 = min(R, r0 + rows_per_cta);
   const double* Ai = a.A.get(item);
   const long long lda = a.A.ld;
-  const int* xi = a.xidx + (long long)item * K;
-  const int* x2 = a.x2idx ? a.x2idx + (long long)item * K : nullptr;
+  const int* xi = a.xidx + (long long)item * a.xstride;
+  const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
   double* pool = a.pool;
 
   for (int e = tid; e < (r1 - r0) * NR; e += SW_THREADS) part[e] = 0.0;
@@ -67,8 +67,8 @@ __global__ void __launch_bounds__(SW_THREADS) gemv_gather_kernel(GemvArgs a, int
     }
   }
   __syncthreads();
-  const int* ai = a.aidx ? a.aidx + (long long)item * R : nullptr;
-  const int* oi = a.oidx + (long long)item * R;
+  const int* ai = a.aidx ? a.aidx + (long long)item * a.ostride : nullptr;
+  const int* oi = a.oidx + (long long)item * a.ostride;
   for (int e = tid; e < (r1 - r0) * NR; e += SW_THREADS) {
     const int rr = e / NR, j = e - rr * NR;
     if (j >= nrhs) continue;
@@ -80,27 +80,36 @@ __global__ void __launch_bounds__(SW_THREADS) gemv_gather_kernel(GemvArgs a, int
 }
 
 // Multi-RHS variant on DMMA tiles: Y (R x NRP) = A (R x K) X (K x NRP), NRP = 8 or 16 padded
-// right-hand sides. Warp tile 16 rows x NRP; A fragments come straight from global memory
-// (each lane group reads 4 consecutive doubles = one 32-byte sector per row), X is staged
-// (gathered) in shared memory with a padded stride so B-fragment loads are conflict free.
-template <int NRP>
-__global__ void __launch_bounds__(128) gemv_dmma_kernel(GemvArgs a, int kchunk, int batch_off) {
+// right-hand sides. A CTA owns rpc rows (16..128) of one item; its 8 warps are split into
+// WR = rpc/16 row groups x WK = 8/WR k-slices (k4 steps dealt round-robin), partial sums are
+// reduced through shared memory. A fragments are streamed straight from global memory (each
+// lane group reads one 32-byte sector per row, 8 loads in flight per lane), X is gathered into
+// shared memory chunk by chunk with a padded stride (conflict-free B fragments).
+template <int NRP, bool VEC>
+__global__ void __launch_bounds__(256) gemv_dmma_kernel(GemvArgs a, int rpc, int kchunk, int batch_off) {
   extern __shared__ double xs[];
-  constexpr int XLD = NRP + 4;
+  // VEC: each lane loads A[r][k+2t .. k+2t+1] as one 16-byte load and uses the two halves as
+  // the A fragments of two "virtual" k4 steps; B fragments follow the same k permutation.
+  // Stride NRP+2 keeps those B loads conflict free, NRP+4 the natural-order ones.
+  constexpr int XLD = VEC ? NRP + 2 : NRP + 4;
   constexpr int NT = NRP / 8;
   const int item = blockIdx.y + batch_off;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
+  const int WR = rpc >> 4, WK = 8 / WR;
+  const int wr = warp % WR, wk = warp / WR;
+  double* red = xs + (size_t)kchunk * XLD;
   const int R = a.R, K = a.K, nrhs = a.nrhs;
-  const int rbase = blockIdx.x * (blockDim.x >> 5) * 16 + warp * 16;
+  const int rbase = blockIdx.x * rpc + wr * 16;
   const double* Ai = a.A.get(item);
   const long long lda = a.A.ld;
-  const int* xi = a.xidx + (long long)item * K;
-  const int* x2 = a.x2idx ? a.x2idx + (long long)item * K : nullptr;
+  const int* xi = a.xidx + (long long)item * a.xstride;
+  const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
   const double* pool = a.pool;
   const int ra = rbase + gq, rb = rbase + 8 + gq;
   const double* rowa = Ai + (long long)(ra < R ? ra : 0) * lda;
   const double* rowb = Ai + (long long)(rb < R ? rb : 0) * lda;
+  const bool la = ra < R, lb = rb < R;
 
   double acc[2][NT][2];
 #pragma unroll
@@ -110,9 +119,9 @@ __global__ void __launch_bounds__(128) gemv_dmma_kernel(GemvArgs a, int kchunk, 
 
   for (int k0 = 0; k0 < K; k0 += kchunk) {
     const int kc = min(kchunk, K - k0);
-    const int kc4 = (kc + 3) & ~3;
+    const int kcp = VEC ? (kc + 7) & ~7 : (kc + 3) & ~3;
     __syncthreads();
-    for (int e = tid; e < kc4 * NRP; e += blockDim.x) {
+    for (int e = tid; e < kcp * NRP; e += blockDim.x) {
       const int k = e / NRP, j = e - k * NRP;
       double v = 0.0;
       if (j < nrhs && k < kc) {
@@ -122,22 +131,103 @@ __global__ void __launch_bounds__(128) gemv_dmma_kernel(GemvArgs a, int kchunk, 
       xs[k * XLD + j] = v;
     }
     __syncthreads();
-#pragma unroll 4
-    for (int k = 0; k < kc4; k += 4) {
-      const int kk = k0 + k + tq;
-      const bool kin = (k + tq) < kc;
-      const double a0 = (kin && ra < R) ? __ldg(rowa + kk) : 0.0;
-      const double a1 = (kin && rb < R) ? __ldg(rowb + kk) : 0.0;
+    if (VEC) {
+      const int step = WK * 8;
+      int k = wk * 8;
+      for (; k < kcp; k += 4 * step) {
+        double2 va[4], vb[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int kk = k + u * step + 2 * tq;
+          va[u] = make_double2(0.0, 0.0);
+          vb[u] = make_double2(0.0, 0.0);
+          if (kk + 1 < kc) {
+            if (la) va[u] = __ldg(reinterpret_cast<const double2*>(rowa + k0 + kk));
+            if (lb) vb[u] = __ldg(reinterpret_cast<const double2*>(rowb + k0 + kk));
+          } else if (kk < kc) {
+            if (la) va[u].x = __ldg(rowa + k0 + kk);
+            if (lb) vb[u].x = __ldg(rowb + k0 + kk);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int kb = k + u * step;
+          if (kb >= kcp) break;
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            const double b0 = xs[(kb + 2 * tq) * XLD + n * 8 + gq];
+            const double b1 = xs[(kb + 2 * tq + 1) * XLD + n * 8 + gq];
+            dmma8x8x4(acc[0][n][0], acc[0][n][1], va[u].x, b0);
+            dmma8x8x4(acc[1][n][0], acc[1][n][1], vb[u].x, b0);
+            dmma8x8x4(acc[0][n][0], acc[0][n][1], va[u].y, b1);
+            dmma8x8x4(acc[1][n][0], acc[1][n][1], vb[u].y, b1);
+          }
+        }
+      }
+      continue;
+    }
+    const int kc4 = kcp;
+    const int step = WK * 4;
+    int k = wk * 4;
+    for (; k + 3 * step < kc4; k += 4 * step) {
+      double va[4], vb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int kk = k + u * step + tq;
+        const bool kin = kk < kc;
+        va[u] = (kin && la) ? __ldg(rowa + k0 + kk) : 0.0;
+        vb[u] = (kin && lb) ? __ldg(rowb + k0 + kk) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const double bv = xs[(k + u * step + tq) * XLD + n * 8 + gq];
+          dmma8x8x4(acc[0][n][0], acc[0][n][1], va[u], bv);
+          dmma8x8x4(acc[1][n][0], acc[1][n][1], vb[u], bv);
+        }
+    }
+    for (; k < kc4; k += step) {
+      const int kk = k + tq;
+      const bool kin = kk < kc;
+      const double va = (kin && la) ? __ldg(rowa + k0 + kk) : 0.0;
+      const double vb = (kin && lb) ? __ldg(rowb + k0 + kk) : 0.0;
 #pragma unroll
       for (int n = 0; n < NT; ++n) {
         const double bv = xs[(k + tq) * XLD + n * 8 + gq];
-        dmma8x8x4(acc[0][n][0], acc[0][n][1], a0, bv);
-        dmma8x8x4(acc[1][n][0], acc[1][n][1], a1, bv);
+        dmma8x8x4(acc[0][n][0], acc[0][n][1], va, bv);
+        dmma8x8x4(acc[1][n][0], acc[1][n][1], vb, bv);
       }
     }
   }
-  const int* ai = a.aidx ? a.aidx + (long long)item * R : nullptr;
-  const int* oi = a.oidx + (long long)item * R;
+  // reduce the k-slices of each row group through shared memory
+  if (WK > 1) {
+    __syncthreads();
+    if (wk > 0) {
+      double* dst = red + ((size_t)((wk - 1) * WR + wr) * 32 + lane) * (4 * NT);
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          dst[(i * NT + n) * 2] = acc[i][n][0];
+          dst[(i * NT + n) * 2 + 1] = acc[i][n][1];
+        }
+    }
+    __syncthreads();
+    if (wk > 0) return;
+    for (int w = 1; w < WK; ++w) {
+      const double* src = red + ((size_t)((w - 1) * WR + wr) * 32 + lane) * (4 * NT);
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          acc[i][n][0] += src[(i * NT + n) * 2];
+          acc[i][n][1] += src[(i * NT + n) * 2 + 1];
+        }
+    }
+  }
+  const int* ai = a.aidx ? a.aidx + (long long)item * a.ostride : nullptr;
+  const int* oi = a.oidx + (long long)item * a.ostride;
   double* pw = a.pool;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
@@ -159,6 +249,150 @@ __global__ void __launch_bounds__(128) gemv_dmma_kernel(GemvArgs a, int kchunk, 
   }
 }
 
+// Staged-x sweep kernel for nrhs <= 2 with an optional fused second stage (tail / chain).
+// Rows are processed by groups of L lanes (L = 4..32 chosen from K so short rows do not idle
+// lanes), 8 independent loads in flight per lane, group-wide shuffle reduction.
+template <int NR, bool VEC>
+__device__ __forceinline__ void rows_dot(const double* __restrict__ A, long long lda, int R, int r0, int r1,
+                                         int K, int L, const double* xs, const int* aidx, const int* oidx,
+                                         double* pool, int nrhs, double* ys) {
+  // each warp streams RB row groups at once (RB x U independent loads in flight per lane)
+  constexpr int RB = 2, U = 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = 32 / L, sub = lane / L, kl = lane % L;
+  const int nw = blockDim.x >> 5;
+  for (int rb = r0 + warp * G * RB; rb < r1; rb += nw * G * RB) {
+    double acc[RB][NR];
+    const double* row[RB];
+    bool live[RB];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      const int r = rb + q * G + sub;
+      live[q] = r < r1;
+      row[q] = A + (long long)(live[q] ? r : r0) * lda;
+#pragma unroll
+      for (int j = 0; j < NR; ++j) acc[q][j] = 0.0;
+    }
+    if (VEC) {
+      // 16-byte loads: lane kl covers columns 2kl, 2kl+1 of each 2L-wide strip
+      for (int k = 2 * kl; k < K; k += 2 * L * U) {
+        double2 v[RB][U];
+#pragma unroll
+        for (int q = 0; q < RB; ++q)
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int kk = k + u * 2 * L;
+            v[q][u] = make_double2(0.0, 0.0);
+            if (live[q]) {
+              if (kk + 1 < K) v[q][u] = __ldg(reinterpret_cast<const double2*>(row[q] + kk));
+              else if (kk < K) v[q][u].x = __ldg(row[q] + kk);
+            }
+          }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int kk = k + u * 2 * L;
+          if (kk >= K) break;
+#pragma unroll
+          for (int j = 0; j < NR; ++j) {
+            const double x0 = xs[kk * NR + j];
+            const double x1 = (kk + 1 < K) ? xs[(kk + 1) * NR + j] : 0.0;
+#pragma unroll
+            for (int q = 0; q < RB; ++q) acc[q][j] = fma(v[q][u].y, x1, fma(v[q][u].x, x0, acc[q][j]));
+          }
+        }
+      }
+    }
+    int k = VEC ? K : kl;
+    for (; k + (U - 1) * L < K; k += U * L) {
+      double v[RB][U];
+#pragma unroll
+      for (int q = 0; q < RB; ++q)
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[q][u] = live[q] ? __ldg(row[q] + k + u * L) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          const double xv = xs[(k + u * L) * NR + j];
+#pragma unroll
+          for (int q = 0; q < RB; ++q) acc[q][j] = fma(v[q][u], xv, acc[q][j]);
+        }
+    }
+    for (; k < K; k += L) {
+#pragma unroll
+      for (int q = 0; q < RB; ++q) {
+        const double v = live[q] ? __ldg(row[q] + k) : 0.0;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) acc[q][j] = fma(v, xs[k * NR + j], acc[q][j]);
+      }
+    }
+#pragma unroll
+    for (int o = L >> 1; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < RB; ++q)
+#pragma unroll
+        for (int j = 0; j < NR; ++j) acc[q][j] += __shfl_xor_sync(0xffffffffu, acc[q][j], o);
+    if (kl == 0) {
+#pragma unroll
+      for (int q = 0; q < RB; ++q) {
+        const int r = rb + q * G + sub;
+        if (!live[q]) continue;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          if (j >= nrhs) break;
+          double y = acc[q][j];
+          if (aidx) y += pool[(long long)aidx[r] * nrhs + j];
+          pool[(long long)oidx[r] * nrhs + j] = y;
+          if (ys) ys[(r - r0) * NR + j] = y;
+        }
+      }
+    }
+  }
+}
+
+__host__ __device__ inline int lanes_for(int K) { return K <= 16 ? 4 : (K <= 48 ? 8 : (K <= 128 ? 16 : 32)); }
+
+template <int NR, bool VEC>
+__global__ void __launch_bounds__(256) sweep_kernel(GemvArgs a, int rows_per_cta, int batch_off) {
+  extern __shared__ double sm[];
+  double* xs = sm;                        // K x NR
+  double* ys = xs + (size_t)a.K * NR;     // R x NR (chain mode)
+  const int item = blockIdx.y + batch_off;
+  const int K = a.K, nrhs = a.nrhs;
+  const int* xi = a.xidx + (long long)item * a.xstride;
+  const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
+  const double* pool = a.pool;
+  for (int e = threadIdx.x; e < K * NR; e += blockDim.x) {
+    const int k = e / NR, j = e - k * NR;
+    double v = 0.0;
+    if (j < nrhs) {
+      v = pool[(long long)xi[k] * nrhs + j];
+      if (x2) v -= pool[(long long)x2[k] * nrhs + j];
+    }
+    xs[e] = v;
+  }
+  __syncthreads();
+  const int r0 = blockIdx.x * rows_per_cta;
+  const int r1 = min(a.R, r0 + rows_per_cta);
+  rows_dot<NR, VEC>(a.A.get(item), a.A.ld, a.R, r0, r1, K, lanes_for(K), xs,
+               a.aidx ? a.aidx + (long long)item * a.ostride : nullptr, a.oidx + (long long)item * a.ostride,
+               a.pool, nrhs, a.mode2 == 2 ? ys : nullptr);
+  if (a.mode2 == 1) {
+    // tail stage rows split evenly over the row chunks of this item
+    const int per = (a.R2 + gridDim.x - 1) / gridDim.x;
+    const int s0 = blockIdx.x * per, s1 = min(a.R2, s0 + per);
+    rows_dot<NR, false>(a.A2.get(item), a.A2.ld, a.R2, s0, s1, a.K2, lanes_for(a.K2), xs + (size_t)(K - a.K2) * NR,
+                 a.a2idx ? a.a2idx + (long long)item * a.R2 : nullptr, a.o2idx + (long long)item * a.R2, a.pool,
+                 nrhs, nullptr);
+  } else if (a.mode2 == 2) {
+    __syncthreads();
+    const double* x2s = ys;
+    rows_dot<NR, false>(a.A2.get(item), a.A2.ld, a.R2, 0, a.R2, a.K2, lanes_for(a.K2), x2s,
+                 a.a2idx ? a.a2idx + (long long)item * a.R2 : nullptr, a.o2idx + (long long)item * a.R2, a.pool,
+                 nrhs, nullptr);
+  }
+}
+
 static int sweep_ctas_target() { return 4 * 148; }
 
 template <int NR>
@@ -177,25 +411,90 @@ static void launch_nr(const GemvArgs& a, cudaStream_t s) {
   }
 }
 
+static bool vec16(const MatB& m) {
+  if (m.ptrs) return false;
+  return (reinterpret_cast<uintptr_t>(m.base + m.off) % 16 == 0) && m.ld % 2 == 0 && m.stride % 2 == 0;
+}
+
 template <int NRP>
 static void launch_dmma(const GemvArgs& a, cudaStream_t s) {
-  int warps = (a.R + 15) / 16;
-  if (warps > 4) warps = 4;
-  const int rows = warps * 16;
-  int kchunk = (48 * 1024 / 8) / (NRP + 4);
-  kchunk &= ~3;
-  const int k4 = (a.K + 3) & ~3;
-  if (kchunk > k4) kchunk = k4;
-  const size_t smem = sizeof(double) * (size_t)kchunk * (NRP + 4);
-  const int gx = (a.R + rows - 1) / rows;
+  const bool vec = false && vec16(a.A);  // 16-byte path measured slower (r01); kept for tuning
+  int rpc = 128;
+  while (rpc > 16 && (rpc >= 2 * a.R || (long long)a.nitems * ((a.R + rpc - 1) / rpc) < 2 * 148)) rpc >>= 1;
+  const int WR = rpc / 16, WK = 8 / WR;
+  const size_t red = (size_t)(WK - 1) * WR * 32 * (4 * (NRP / 8));
+  const int xld = vec ? NRP + 2 : NRP + 4;
+  int kchunk = (int)((48 * 1024 / 8 - red) / xld) & ~7;
+  const int k8 = (a.K + 7) & ~7;
+  if (kchunk > k8) kchunk = k8;
+  const size_t smem = sizeof(double) * ((size_t)kchunk * xld + red);
+  const int gx = (a.R + rpc - 1) / rpc;
   for (int off = 0; off < a.nitems; off += 65535) {
     dim3 grid(gx, min(65535, a.nitems - off));
-    gemv_dmma_kernel<NRP><<<grid, warps * 32, smem, s>>>(a, kchunk, off);
+    if (vec)
+      gemv_dmma_kernel<NRP, true><<<grid, 256, smem, s>>>(a, rpc, kchunk, off);
+    else
+      gemv_dmma_kernel<NRP, false><<<grid, 256, smem, s>>>(a, rpc, kchunk, off);
   }
+}
+
+template <int NR>
+static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
+  const size_t smem = sizeof(double) * NR * ((size_t)a.K + (a.mode2 == 2 ? a.R : 0));
+  if (smem > 48 * 1024) return false;
+  int rows = a.R;
+  if (a.mode2 != 2) {
+    const int G = 32 / lanes_for(a.K);
+    const int minrows = 8 * G * 2;
+    rows = a.R < 64 ? a.R : 64;
+    while (rows > minrows && (long long)a.nitems * ((a.R + rows - 1) / rows) < 4 * 148) rows = (rows + 1) / 2;
+    if (rows < minrows) rows = minrows < a.R ? minrows : a.R;
+  }
+  const int gx = (a.R + rows - 1) / rows;
+  const bool vec = false && vec16(a.A);  // 16-byte path measured slower (r01); kept for tuning
+  for (int off = 0; off < a.nitems; off += 65535) {
+    dim3 grid(gx, min(65535, a.nitems - off));
+    if (vec)
+      sweep_kernel<NR, true><<<grid, 256, smem, s>>>(a, rows, off);
+    else
+      sweep_kernel<NR, false><<<grid, 256, smem, s>>>(a, rows, off);
+  }
+  return true;
 }
 
 int launch_gemv_gather(const GemvArgs& a, cudaStream_t s) {
   if (a.nitems <= 0 || a.R <= 0) return 0;
+  if (a.nrhs <= 2) {
+    const bool ok = a.nrhs == 1 ? launch_sweep<1>(a, s) : launch_sweep<2>(a, s);
+    if (ok) return cudaGetLastError() == cudaSuccess ? 0 : 2;
+  }
+  if (a.mode2) {
+    // second stage for the chunked / multi-RHS paths: separate launch after the first
+    GemvArgs b = a;
+    b.mode2 = 0;
+    int rc = launch_gemv_gather(b, s);
+    if (rc) return rc;
+    GemvArgs c{};
+    c.nitems = a.nitems;
+    c.nrhs = a.nrhs;
+    c.pool = a.pool;
+    c.A = a.A2;
+    c.R = a.R2;
+    c.K = a.K2;
+    c.aidx = a.a2idx;
+    c.oidx = a.o2idx;
+    c.ostride = a.R2;
+    if (a.mode2 == 1) {
+      // tail: the last K2 gather indices of the first stage (no difference operand)
+      if (a.x2idx) return 1;
+      c.xidx = a.xidx + (a.K - a.K2);
+      c.xstride = a.xstride;
+    } else {
+      c.xidx = a.oidx;  // chain: x of the second stage = y1 rows in the pool
+      c.xstride = a.ostride;
+    }
+    return launch_gemv_gather(c, s);
+  }
   if (a.nrhs <= 1)
     launch_nr<1>(a, s);
   else if (a.nrhs <= 2)

@@ -318,33 +318,31 @@ class FactorizedSolver:
         if prog is not None:
             return prog
         lay = self._layout
-        pool = torch.zeros((lay["rows"], nrhs), dtype=torch.float64, device=self.device)
         keep = []
 
-        def gemv(nitems, R, K, A, xidx, oidx, x2idx=None, aidx=None):
-            xi = _i32(xidx, self.device)
-            oi = _i32(oidx, self.device)
-            x2 = None if x2idx is None else _i32(x2idx, self.device)
-            ai = None if aidx is None else _i32(aidx, self.device)
-            keep.extend([xi, oi, x2, ai])
-            return _ext.GemvBatch(nitems, R, K, nrhs, A, pool.data_ptr(), xi.data_ptr(), _ext.ptr(x2),
-                                  _ext.ptr(ai), oi.data_ptr())
+        def gemv(nitems, R, K, A, xidx, oidx, x2idx=None, aidx=None, mode2=0, R2=0, K2=0, A2=None,
+                 o2idx=None, a2idx=None):
+            return dict(nitems=nitems, R=R, K=K, A=A, xidx=np.asarray(xidx), oidx=np.asarray(oidx),
+                        x2idx=None if x2idx is None else np.asarray(x2idx),
+                        aidx=None if aidx is None else np.asarray(aidx), mode2=mode2, R2=R2, K2=K2, A2=A2,
+                        o2idx=None if o2idx is None else np.asarray(o2idx),
+                        a2idx=None if a2idx is None else np.asarray(a2idx))
 
         up, down = [], []
         p, q = self.p, self.q
         m, b, P, c = (p - 2) ** 2, 4 * q, p * p, 4 * (p - 1)
         hslot = lay["hslot"]
         tree, plan = self.tree, self.plan
-        # leaves: h = H g
+        # leaves: h = H g   (solver.py:278)
         for grp in self.leaf_groups:
             L = len(grp.ids)
             rows = grp.first_row + np.arange(L)
             xidx = lay["G"] + rows[:, None] * m + np.arange(m)[None, :]
             oidx = np.stack([hslot[n] + np.arange(b) for n in grp.ids])
             up.append(gemv(L, b, m, _ext.mat(grp.h, b * m, m), xidx, oidx))
-        # parents, deepest first
+        # parents, deepest first: w3 = X (h_b[p3b] - h_a[p3a]); h = T_ei w3 + [h_a[p1a]; h_b[p2b]]
         for grp in sorted(self.parent_groups, key=lambda g_: -g_.depth):
-            m3, e, n1 = grp.m3, grp.e, grp.n1
+            m3, e = grp.m3, grp.e
             xw, x2w, ow, ah, oh = [], [], [], [], []
             for nid in grp.ids:
                 ca, cb = tree.nodes[nid].children
@@ -360,14 +358,21 @@ class FactorizedSolver:
                 xmat = _ext.mat(grp.wrap["xsw"], m3 * ldx, ldx)
             else:
                 xmat = _ext.mat(grp.xs, m3 * (m3 + e), m3 + e)
-            up.append(gemv(nI, m3, m3, xmat, np.stack(xw), np.stack(ow), x2idx=np.stack(x2w)))
-            up.append(gemv(nI, e, m3, _ext.mat(grp.tei, e * m3, m3), np.stack(ow), np.stack(oh), aidx=np.stack(ah)))
+            teim = _ext.mat(grp.tei, e * m3, m3)
+            per_item = m3 * m3 + e * m3
+            if nI >= 296 or per_item <= 32768:
+                # one launch: the chained second stage reads w3 from shared memory
+                up.append(gemv(nI, m3, m3, xmat, np.stack(xw), np.stack(ow), x2idx=np.stack(x2w),
+                               mode2=2, R2=e, K2=m3, A2=teim, o2idx=np.stack(oh), a2idx=np.stack(ah)))
+            else:
+                up.append(gemv(nI, m3, m3, xmat, np.stack(xw), np.stack(ow), x2idx=np.stack(x2w)))
+                up.append(gemv(nI, e, m3, teim, np.stack(ow), np.stack(oh), aidx=np.stack(ah)))
             if grp.wrap is not None:
                 nid = grp.ids[0]
                 ec = grp.wrap["ec"]
                 up.append(gemv(1, ec, e, _ext.mat(grp.wrap["qd_dev"], 0, e),
                                (lay["hpre"][nid] + np.arange(e))[None], (hslot[nid] + np.arange(ec))[None]))
-        # downward: parents root first
+        # downward: parents root first: u[j3] = S u_ext + w[j3]   (solver.py:329-335)
         for grp in sorted(self.parent_groups, key=lambda g_: g_.depth):
             m3, e = grp.m3, grp.e
             if grp.wrap is not None:
@@ -384,7 +389,7 @@ class FactorizedSolver:
             j3 = np.stack([plan.node[n].j3 for n in grp.ids])
             down.append(gemv(len(grp.ids), m3, e, _ext.mat(grp.xs, m3 * (m3 + e), m3 + e, off=m3), xi,
                              lay["U"] + j3, aidx=lay["W"] + j3))
-        # leaves: u_c[i_ci] = [F | S] [g; u_ext],  u_c[i_ce] = L u_ext
+        # leaves: u_c[i_ci] = [F | S] [g; u_ext], fused tail stage u_c[i_ce] = L u_ext  (solver.py:325-327)
         for grp in self.leaf_groups:
             L = len(grp.ids)
             rows = grp.first_row + np.arange(L)
@@ -392,8 +397,66 @@ class FactorizedSolver:
             gx = lay["G"] + rows[:, None] * m + np.arange(m)[None, :]
             base = lay["UC"] + rows[:, None] * P
             down.append(gemv(L, m, m + b, _ext.mat(grp.fs, m * (m + b), m + b), np.concatenate([gx, ext], axis=1),
-                             base + grp.sc.i_ci[None, :]))
-            down.append(gemv(L, c, b, _ext.mat(grp.consts["lift"], 0, b), ext, base + grp.sc.i_ce[None, :]))
+                             base + grp.sc.i_ci[None, :], mode2=1, R2=c, K2=b,
+                             A2=_ext.mat(grp.consts["lift"], 0, b), o2idx=base + grp.sc.i_ce[None, :]))
+        # split-K for steps with long rows and too few CTAs (top of the tree): partial products
+        # into scratch pool rows, then a deterministic reduction step (A = ones)
+        scratch = [lay["rows"]]
+
+        def split(spec):
+            if spec["mode2"] or spec["K"] < 512:
+                return [spec]
+            rows_min = 16 if nrhs > 2 else 8
+            ctas = spec["nitems"] * -(-spec["R"] // rows_min)
+            if ctas >= 600:
+                return [spec]
+            K = spec["K"]
+            want = min(-(-600 // ctas), K // 128)
+            ns = max([d for d in range(1, want + 1) if K % d == 0] or [1])
+            if ns <= 1:
+                return [spec]
+            kc = K // ns
+            A, n, R = spec["A"], spec["nitems"], spec["R"]
+            base = A.base if A.base else 0
+            ptrs = np.array([base + 8 * (i * A.stride + A.off + s * kc) for i in range(n) for s in range(ns)],
+                            dtype=np.int64)
+            ptr_t = torch.as_tensor(ptrs, device=self.device)
+            keep.append(ptr_t)
+            scr0 = scratch[0]
+            scratch[0] += n * ns * R
+            t = np.arange(n * ns)
+            part = dict(spec)
+            part.update(nitems=n * ns, K=kc, A=_ext.MatBatch(0, 0, ptr_t.data_ptr(), A.ld, 0),
+                        xidx=spec["xidx"].reshape(n, ns, kc).reshape(n * ns, kc),
+                        x2idx=None if spec["x2idx"] is None else spec["x2idx"].reshape(n * ns, kc),
+                        aidx=None, oidx=scr0 + t[:, None] * R + np.arange(R)[None, :])
+            ones = torch.ones(ns, dtype=torch.float64, device=self.device)
+            keep.append(ones)
+            ii, rr = np.divmod(np.arange(n * R), R)
+            red = dict(nitems=n * R, R=1, K=ns, A=_ext.mat(ones, 0, ns),
+                       xidx=scr0 + ((ii[:, None] * ns + np.arange(ns)[None, :]) * R + rr[:, None]),
+                       x2idx=None, oidx=spec["oidx"].reshape(n * R, 1),
+                       aidx=None if spec["aidx"] is None else spec["aidx"].reshape(n * R, 1),
+                       mode2=0, R2=0, K2=0, A2=None, o2idx=None, a2idx=None)
+            return [part, red]
+
+        up = [s2 for s1 in up for s2 in split(s1)]
+        down = [s2 for s1 in down for s2 in split(s1)]
+        pool = torch.zeros((scratch[0], nrhs), dtype=torch.float64, device=self.device)
+
+        def build(spec):
+            dev = self.device
+            arrs = [_i32(spec[k], dev) if spec[k] is not None else None
+                    for k in ("xidx", "oidx", "x2idx", "aidx", "o2idx", "a2idx")]
+            keep.extend(arrs)
+            xi, oi, x2, ai, o2, a2 = arrs
+            A2 = spec["A2"] if spec["A2"] is not None else _ext.MatBatch()
+            return _ext.GemvBatch(spec["nitems"], spec["R"], spec["K"], nrhs, spec["A"], pool.data_ptr(),
+                                  xi.data_ptr(), _ext.ptr(x2), _ext.ptr(ai), oi.data_ptr(), spec["mode2"],
+                                  spec["R2"], spec["K2"], A2, _ext.ptr(a2), _ext.ptr(o2))
+
+        up = [build(s_) for s_ in up]
+        down = [build(s_) for s_ in down]
         root_rows = torch.as_tensor(lay["U"] + plan.node[tree.root].ext, dtype=torch.long, device=self.device)
         f_in = torch.zeros((root_rows.numel(), nrhs), dtype=torch.float64, device=self.device)
         prog = {"pool": pool, "up": up, "down": down, "keep": keep, "root_rows": root_rows, "f_in": f_in,

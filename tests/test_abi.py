@@ -25,7 +25,7 @@ def test_library_loads_and_exports():
     for name in declared_symbols():
         assert hasattr(lib, name), name
     lib.hps_abi_version.restype = ctypes.c_int
-    assert lib.hps_abi_version() == 1
+    assert lib.hps_abi_version() == _ext.ABI_VERSION
     # workspace queries are host-only arithmetic
     lib.hps_leaf_workspace_bytes.restype = ctypes.c_longlong
     assert lib.hps_leaf_workspace_bytes(4, 16, 15) > 0

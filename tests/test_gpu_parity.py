@@ -123,3 +123,41 @@ def test_resonant_leaf_raises():
     tree = build_uniform_tree(UNIT, 1)
     with pytest.raises(LeafSingularError, match="singular"):
         build_stage(tree, catalog("helmholtz", kappa=np.sqrt(2.0) * np.pi), 20, 19)
+
+
+@pytest.mark.parametrize("nrhs,n,p", [(1, 4, 10), (2, 4, 10), (3, 4, 10), (8, 4, 10), (16, 4, 10), (16, 16, 12)])
+def test_multi_rhs_device_solve_matches_single(nrhs, n, p):
+    import torch
+    tree = build_uniform_tree(UNIT, n)
+    refine_near_point(tree, (0.5, 0.5), 1)
+    spec = catalog("varcoef_helmholtz", kappa=10.0)
+    solver = build_stage(tree, spec, p, p - 2)
+    m = (p - 2) ** 2
+    nl = solver._n_leaves
+    rng = np.random.default_rng(nrhs)
+    root_ext = solver.plan.node[tree.root].ext
+    F = rng.standard_normal((root_ext.size, nrhs))
+    G = rng.standard_normal((nl * m, nrhs))
+    out = solver.solve_device(torch.tensor(F, device="cuda"), torch.tensor(G, device="cuda"))
+    u = out["u"].cpu().numpy()
+    uc = out["uc"].cpu().numpy()
+    for j in range(nrhs):
+        st = solver.solve(f=F[:, j], g=G[:, j].reshape(nl, m))
+        assert rel_maxdiff(u[:, j], st.u) <= 1e-12
+        ref = np.stack([st.leaf_solutions[i] for i in solver._leaf_ids])
+        assert rel_maxdiff(uc[:, :, j], ref) <= 1e-12
+
+
+def test_upward_downward_split_matches_solve():
+    from paper_1612_02736_b200 import downward_pass, upward_pass
+    spec = catalog("manufactured", u="sin(pi*x1)*sin(pi*x2)")
+    tree = build_uniform_tree(UNIT, 2)
+    solver = build_stage(tree, spec, 17, 16)
+    st = upward_pass(solver)
+    assert np.abs(st.u).max() == 0.0
+    j3 = solver.plan.node[tree.root].j3
+    pts = solver.plan.coords[j3]
+    np.testing.assert_allclose(st.w[j3], np.sin(np.pi * pts[:, 0]) * np.sin(np.pi * pts[:, 1]), atol=1e-9)
+    full = downward_pass(solver, None, st)
+    ref = solver.solve()
+    assert rel_maxdiff(full.u, ref.u) <= 1e-14
