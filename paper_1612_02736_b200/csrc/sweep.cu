@@ -8,6 +8,8 @@
 //   parent down  u[j3]  = S u[ext] + w[j3]                        (solver.py:335)
 //   leaf down    u_c    = [F_ii | S_ie] [g; u_ge],  u_ce = L u_ge  (solver.py:325-327)
 // Bandwidth-bound: each operator entry is read once per call and used for nrhs FMAs.
+#include <cstdlib>
+
 #include "hps_common.cuh"
 #include "hps_kernels.cuh"
 
@@ -34,6 +36,13 @@ __global__ void __launch_bounds__(SW_THREADS) gemv_gather_kernel(GemvArgs a, int
   double* pool = a.pool;
 
   for (int e = tid; e < (r1 - r0) * NR; e += SW_THREADS) part[e] = 0.0;
+  for (int r = r0 + tid; r < r1; r += SW_THREADS) {
+    // start streaming this CTA's operator rows into L2 while x is gathered
+    const double* rp = Ai + (long long)r * lda;
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(rp) & ~(uintptr_t)15;
+    const uintptr_t hi = (reinterpret_cast<uintptr_t>(rp + K) + 15) & ~(uintptr_t)15;
+    prefetch_l2_bulk(reinterpret_cast<const void*>(lo), (unsigned)(hi - lo));
+  }
 
   for (int k0 = 0; k0 < K; k0 += kchunk) {
     const int kc = min(kchunk, K - k0);
@@ -252,12 +261,11 @@ __global__ void __launch_bounds__(256) gemv_dmma_kernel(GemvArgs a, int rpc, int
 // Staged-x sweep kernel for nrhs <= 2 with an optional fused second stage (tail / chain).
 // Rows are processed by groups of L lanes (L = 4..32 chosen from K so short rows do not idle
 // lanes), 8 independent loads in flight per lane, group-wide shuffle reduction.
-template <int NR, bool VEC>
+template <int NR, bool VEC, int RB = 2, int U = 4>
 __device__ __forceinline__ void rows_dot(const double* __restrict__ A, long long lda, int R, int r0, int r1,
                                          int K, int L, const double* xs, const int* aidx, const int* oidx,
                                          double* pool, int nrhs, double* ys) {
   // each warp streams RB row groups at once (RB x U independent loads in flight per lane)
-  constexpr int RB = 2, U = 4;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = 32 / L, sub = lane / L, kl = lane % L;
   const int nw = blockDim.x >> 5;
@@ -352,7 +360,7 @@ __device__ __forceinline__ void rows_dot(const double* __restrict__ A, long long
 
 __host__ __device__ inline int lanes_for(int K) { return K <= 16 ? 4 : (K <= 48 ? 8 : (K <= 128 ? 16 : 32)); }
 
-template <int NR, bool VEC>
+template <int NR, bool VEC, int RB = 2, int U = 4>
 __global__ void __launch_bounds__(256) sweep_kernel(GemvArgs a, int rows_per_cta, int batch_off) {
   extern __shared__ double sm[];
   double* xs = sm;                        // K x NR
@@ -362,6 +370,17 @@ __global__ void __launch_bounds__(256) sweep_kernel(GemvArgs a, int rows_per_cta
   const int* xi = a.xidx + (long long)item * a.xstride;
   const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
   const double* pool = a.pool;
+  {
+    // start streaming this CTA's operator rows into L2 while x is gathered
+    const int p0 = blockIdx.x * rows_per_cta, p1 = min(a.R, p0 + rows_per_cta);
+    const double* Ai = a.A.get(item);
+    for (int r = p0 + threadIdx.x; r < p1; r += blockDim.x) {
+      const double* rp = Ai + (long long)r * a.A.ld;
+      const uintptr_t lo = reinterpret_cast<uintptr_t>(rp) & ~(uintptr_t)15;
+      const uintptr_t hi = (reinterpret_cast<uintptr_t>(rp + K) + 15) & ~(uintptr_t)15;
+      prefetch_l2_bulk(reinterpret_cast<const void*>(lo), (unsigned)(hi - lo));
+    }
+  }
   for (int e = threadIdx.x; e < K * NR; e += blockDim.x) {
     const int k = e / NR, j = e - k * NR;
     double v = 0.0;
@@ -374,7 +393,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(GemvArgs a, int rows_per_cta
   __syncthreads();
   const int r0 = blockIdx.x * rows_per_cta;
   const int r1 = min(a.R, r0 + rows_per_cta);
-  rows_dot<NR, VEC>(a.A.get(item), a.A.ld, a.R, r0, r1, K, lanes_for(K), xs,
+  rows_dot<NR, VEC, RB, U>(a.A.get(item), a.A.ld, a.R, r0, r1, K, lanes_for(K), xs,
                a.aidx ? a.aidx + (long long)item * a.ostride : nullptr, a.oidx + (long long)item * a.ostride,
                a.pool, nrhs, a.mode2 == 2 ? ys : nullptr);
   if (a.mode2 == 1) {
@@ -440,6 +459,14 @@ static void launch_dmma(const GemvArgs& a, cudaStream_t s) {
 
 template <int NR>
 static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
+  {
+    static int old = -1;
+    if (old < 0) {
+      const char* e = getenv("HPS_SWEEP_VARIANT");
+      old = (e && atoi(e) != 9) ? 0 : 1;  // default: previous gemv_gather kernel for single-stage steps
+    }
+    if (old && !a.mode2) return false;  // variant 9: previous gemv_gather kernel
+  }
   const size_t smem = sizeof(double) * NR * ((size_t)a.K + (a.mode2 == 2 ? a.R : 0));
   if (smem > 48 * 1024) return false;
   int rows = a.R;
@@ -451,13 +478,20 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
     if (rows < minrows) rows = minrows < a.R ? minrows : a.R;
   }
   const int gx = (a.R + rows - 1) / rows;
-  const bool vec = false && vec16(a.A);  // 16-byte path measured slower (r01); kept for tuning
+  static int variant = -1;
+  if (variant < 0) {
+    const char* e = getenv("HPS_SWEEP_VARIANT");
+    variant = e ? atoi(e) : 0;
+  }
   for (int off = 0; off < a.nitems; off += 65535) {
     dim3 grid(gx, min(65535, a.nitems - off));
-    if (vec)
-      sweep_kernel<NR, true><<<grid, 256, smem, s>>>(a, rows, off);
-    else
-      sweep_kernel<NR, false><<<grid, 256, smem, s>>>(a, rows, off);
+    switch (variant) {
+      case 1: sweep_kernel<NR, false, 1, 8><<<grid, 256, smem, s>>>(a, rows, off); break;
+      case 2: sweep_kernel<NR, true, 1, 4><<<grid, 256, smem, s>>>(a, rows, off); break;
+      case 3: sweep_kernel<NR, false, 1, 4><<<grid, 256, smem, s>>>(a, rows, off); break;
+      case 4: sweep_kernel<NR, true, 2, 2><<<grid, 256, smem, s>>>(a, rows, off); break;
+      default: sweep_kernel<NR, false, 2, 4><<<grid, 256, smem, s>>>(a, rows, off); break;
+    }
   }
   return true;
 }

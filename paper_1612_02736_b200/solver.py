@@ -406,6 +406,8 @@ class FactorizedSolver:
         def split(spec):
             if spec["mode2"] or spec["K"] < 512:
                 return [spec]
+            if nrhs <= 2 and 8 * spec["nitems"] * spec["R"] * spec["K"] < 64e6:
+                return [spec]  # single-RHS: the extra reduction launch costs more than it saves
             rows_min = 16 if nrhs > 2 else 8
             ctas = spec["nitems"] * -(-spec["R"] // rows_min)
             if ctas >= 600:
