@@ -110,6 +110,7 @@ class _LeafGroup:
     ainvnorm: torch.Tensor = None
     status: torch.Tensor = None
     consts: dict = None
+    coef: torch.Tensor = None  # [6, L, P] coefficient samples (kept only in economy mode)
     first_row: int = 0     # global leaf row of slot 0 (G / UC regions)
 
 
@@ -298,6 +299,15 @@ class FactorizedSolver:
             _ext.check(lib.hps_sweep_gemv(step, s), "downward sweep")
 
     def _execute(self, prog, down=True):
+        if self.mode == "econ":
+            lib = _ext.load()
+            s = _stream_ptr()
+            fresh = [_leaf_build_call(grp, self.p, self.q, lib, s) for grp in self.leaf_groups]
+            for pas, i, (kind, gi) in prog["patches"]:
+                prog[pas][i].A.base = (fresh[gi][0] if kind == "fs" else fresh[gi][1]).data_ptr()
+            self._steps(prog, down)
+            del fresh  # stream-ordered: the allocator reuses the blocks only for later work
+            return
         if not (down and self.use_graphs):
             self._steps(prog, down)
             return
@@ -339,7 +349,8 @@ class FactorizedSolver:
             rows = grp.first_row + np.arange(L)
             xidx = lay["G"] + rows[:, None] * m + np.arange(m)[None, :]
             oidx = np.stack([hslot[n] + np.arange(b) for n in grp.ids])
-            up.append(gemv(L, b, m, _ext.mat(grp.h, b * m, m), xidx, oidx))
+            up.append(gemv(L, b, m, _ext.mat(grp.h if grp.h is not None else 0, b * m, m), xidx, oidx))
+            up[-1]["patch"] = ("h", self.leaf_groups.index(grp))
         # parents, deepest first: w3 = X (h_b[p3b] - h_a[p3a]); h = T_ei w3 + [h_a[p1a]; h_b[p2b]]
         for grp in sorted(self.parent_groups, key=lambda g_: -g_.depth):
             m3, e = grp.m3, grp.e
@@ -396,9 +407,11 @@ class FactorizedSolver:
             ext = np.stack([lay["U"] + plan.node[n].ext for n in grp.ids])
             gx = lay["G"] + rows[:, None] * m + np.arange(m)[None, :]
             base = lay["UC"] + rows[:, None] * P
-            down.append(gemv(L, m, m + b, _ext.mat(grp.fs, m * (m + b), m + b), np.concatenate([gx, ext], axis=1),
+            down.append(gemv(L, m, m + b, _ext.mat(grp.fs if grp.fs is not None else 0, m * (m + b), m + b),
+                             np.concatenate([gx, ext], axis=1),
                              base + grp.sc.i_ci[None, :], mode2=1, R2=c, K2=b,
                              A2=_ext.mat(grp.consts["lift"], 0, b), o2idx=base + grp.sc.i_ce[None, :]))
+            down[-1]["patch"] = ("fs", self.leaf_groups.index(grp))
         # split-K for steps with long rows and too few CTAs (top of the tree): partial products
         # into scratch pool rows, then a deterministic reduction step (A = ones)
         scratch = [lay["rows"]]
@@ -457,12 +470,14 @@ class FactorizedSolver:
                                   xi.data_ptr(), _ext.ptr(x2), _ext.ptr(ai), oi.data_ptr(), spec["mode2"],
                                   spec["R2"], spec["K2"], A2, _ext.ptr(a2), _ext.ptr(o2))
 
+        patches = [(k, i, s_["patch"]) for k, lst in (("up", up), ("down", down))
+                   for i, s_ in enumerate(lst) if "patch" in s_]
         up = [build(s_) for s_ in up]
         down = [build(s_) for s_ in down]
         root_rows = torch.as_tensor(lay["U"] + plan.node[tree.root].ext, dtype=torch.long, device=self.device)
         f_in = torch.zeros((root_rows.numel(), nrhs), dtype=torch.float64, device=self.device)
         prog = {"pool": pool, "up": up, "down": down, "keep": keep, "root_rows": root_rows, "f_in": f_in,
-                "graph": None}
+                "graph": None, "patches": patches}
         self._sweeps[nrhs] = prog
         return prog
 
@@ -529,8 +544,6 @@ def build_stage(tree, spec, p: int, q: int, mode: str = "stored", plan=None, ord
         raise ValueError(f"unknown mode {mode!r}")
     if p < q + 1:
         raise ValueError(f"leaf order must satisfy p >= q+1, got p={p}, q={q}")
-    if mode == "econ":
-        raise NotImplementedError("economy mode is not implemented on the GPU path yet")
     t0 = time.perf_counter()
     if plan is None:
         plan = enumerate_gauss_nodes(tree, q)
@@ -609,21 +622,12 @@ def _build_device(solver: FactorizedSolver, order, profile=False):
             bnd = tree.nodes[ids[bad]].bounds
             raise ValueError(f"non-finite coefficient evaluation on leaf "
                              f"{(bnd.x1lo, bnd.x1hi, bnd.x2lo, bnd.x2hi)}")
-        grp.fs = torch.empty((L, m, m + b), dtype=torch.float64, device=dev)
-        grp.h = torch.empty((L, b, m), dtype=torch.float64, device=dev)
-        t_maps = torch.empty((L, b, b), dtype=torch.float64, device=dev)
         grp.anorm = torch.empty(L, dtype=torch.float64, device=dev)
         grp.ainvnorm = torch.empty(L, dtype=torch.float64, device=dev)
         grp.status = torch.zeros(L, dtype=torch.int32, device=dev)
-        ws = torch.empty(int(lib.hps_leaf_workspace_bytes(L, p, q)), dtype=torch.uint8, device=dev)
-        cs = grp.consts
-        lb = _ext.LeafBatch(L, p, q, coef.data_ptr(), cs["dx"].data_ptr(), cs["dy"].data_ptr(),
-                            cs["dxx"].data_ptr(), cs["dyy"].data_ptr(), cs["int_pos"].data_ptr(),
-                            cs["ext_pos"].data_ptr(), cs["lift"].data_ptr(), cs["dfi"].data_ptr(),
-                            cs["t0"].data_ptr(), grp.fs.data_ptr(), grp.h.data_ptr(), t_maps.data_ptr(),
-                            grp.anorm.data_ptr(), grp.ainvnorm.data_ptr(), grp.status.data_ptr(), ws.data_ptr())
+        grp.coef = coef
         ph.mark(f"leaf-prep {key}")
-        _ext.check(lib.hps_leaf_build(lb, s), "leaf build")
+        grp.fs, grp.h, t_maps = _leaf_build_call(grp, p, q, lib, s)
         ph.mark(f"leaf-build {key} x{L}")
         for slot, nid in enumerate(ids):
             tloc[nid] = (t_maps, slot * b * b, b)
@@ -692,7 +696,33 @@ def _build_device(solver: FactorizedSolver, order, profile=False):
     ph.mark("merges-done")
     _finish_checks(solver, order)
     solver.phase_ms = ph.report()
+    for grp in solver.leaf_groups:
+        if solver.mode == "econ":
+            # economy mode (reference leaf.py:156-157, solver.py:262-271,317-323): nothing is
+            # retained per leaf but the coefficient samples; every solve re-runs the leaf stage
+            grp.fs = grp.h = None
+        else:
+            grp.coef = None
     solver._layout = _layout(solver)
+
+
+def _leaf_build_call(grp, p, q, lib, s):
+    """One hps_leaf_build for a leaf group; returns fresh (fs, h, t) device tensors."""
+    dev = grp.coef.device
+    L = len(grp.ids)
+    m, b = (p - 2) ** 2, 4 * q
+    fs = torch.empty((L, m, m + b), dtype=torch.float64, device=dev)
+    h = torch.empty((L, b, m), dtype=torch.float64, device=dev)
+    t = torch.empty((L, b, b), dtype=torch.float64, device=dev)
+    ws = torch.empty(int(lib.hps_leaf_workspace_bytes(L, p, q)), dtype=torch.uint8, device=dev)
+    cs = grp.consts
+    lb = _ext.LeafBatch(L, p, q, grp.coef.data_ptr(), cs["dx"].data_ptr(), cs["dy"].data_ptr(),
+                        cs["dxx"].data_ptr(), cs["dyy"].data_ptr(), cs["int_pos"].data_ptr(),
+                        cs["ext_pos"].data_ptr(), cs["lift"].data_ptr(), cs["dfi"].data_ptr(),
+                        cs["t0"].data_ptr(), fs.data_ptr(), h.data_ptr(), t.data_ptr(),
+                        grp.anorm.data_ptr(), grp.ainvnorm.data_ptr(), grp.status.data_ptr(), ws.data_ptr())
+    _ext.check(lib.hps_leaf_build(lb, s), "leaf build")
+    return fs, h, t
 
 
 def _apply_wrap(solver, grp, en, lib, s):

@@ -161,3 +161,39 @@ def test_upward_downward_split_matches_solve():
     full = downward_pass(solver, None, st)
     ref = solver.solve()
     assert rel_maxdiff(full.u, ref.u) <= 1e-14
+
+
+class TestEconomyMode:
+    """Reference test_solver.py:226-247,284-292 (econ == stored, memory strictly smaller)."""
+
+    def test_solutions_match_stored(self):
+        spec = catalog("varcoef_helmholtz", kappa=8.0)
+        tree = build_uniform_tree(UNIT, 4)
+        stored = build_stage(tree, spec, 9, 8, "stored")
+        econ = build_stage(tree, spec, 9, 8, "econ")
+        s, e = stored.solve(), econ.solve()
+        assert np.abs(s.u - e.u).max() <= 1e-12
+        for nid in s.leaf_solutions:
+            np.testing.assert_allclose(s.leaf_solutions[nid], e.leaf_solutions[nid], atol=1e-12)
+
+    def test_memory_strictly_smaller(self):
+        tree = build_uniform_tree(UNIT, 4)
+        stored = build_stage(tree, catalog("laplace"), 9, 8, "stored")
+        econ = build_stage(tree, catalog("laplace"), 9, 8, "econ")
+        assert econ.memory_floats() < stored.memory_floats()
+        assert econ.leaf_memory_floats() == 0 and stored.leaf_memory_floats() > 0
+        assert econ.device_bytes() < stored.device_bytes()
+
+    def test_econ_on_refined_mesh_and_repeat(self):
+        spec = catalog("manufactured", u="sin(pi*x1)*sin(pi*x2)")
+        tree = build_uniform_tree(UNIT, 4)
+        refine_near_point(tree, (0.5, 0.5), 1)
+        us = build_stage(tree, spec, 9, 8, "stored").solve().u
+        econ = build_stage(tree, spec, 9, 8, "econ")
+        ue1, ue2 = econ.solve().u, econ.solve().u
+        assert np.abs(us - ue1).max() <= 1e-12
+        np.testing.assert_array_equal(ue1, ue2)
+
+    def test_unknown_mode(self):
+        with pytest.raises(ValueError, match="unknown mode"):
+            build_stage(build_uniform_tree(UNIT, 1), catalog("laplace"), 9, 8, mode="compressed")
