@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(128) gemm_dmma_kernel(GemmArgs g, int batch_of
   const int lda = g.A.ld, ldb = g.B.ld, ldc = g.C.ld;
   const int M = g.M, N = g.N, K = g.K;
 
-  auto colmap = [&](int c) { return (MODE == MODE_GJ_UPD && c >= g.k0) ? c + g.kb : c; };
+  auto colmap = [&](int c) { return (MODE == MODE_GJ_UPD && c >= g.kc) ? c + g.kb : c; };
 
   auto load_tile = [&](int stage, int k) {
     // A: 64 rows x 16 k  -> 1024 elements, 8 per thread; consecutive threads walk k
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(BigCfg<BN>::THREADS, BigCfg<BN>::MINB) gemm_bi
   double* C = g.C.get(item);
   const long long lda = g.A.ld, ldb = g.B.ld, ldc = g.C.ld;
   const int M = g.M, N = g.N, K = g.K;
-  auto colmap = [&](int c) { return (MODE == MODE_GJ_UPD && c >= g.k0) ? c + g.kb : c; };
+  auto colmap = [&](int c) { return (MODE == MODE_GJ_UPD && c >= g.kc) ? c + g.kb : c; };
 
   auto load_tile = [&](int stage, int k) {
     double* as = As + stage * BA_STAGE;
@@ -321,7 +321,7 @@ template <int MODE, int BN>
 static void launch_big(const GemmArgs& g, int batch, cudaStream_t s) {
   using Cfg = BigCfg<BN>;
   const bool vec = aligned16(g.A) && aligned16(g.B) && aligned16(g.C) &&
-                   (MODE != MODE_GJ_UPD || (g.k0 % 2 == 0 && g.kb % 2 == 0));
+                   (MODE != MODE_GJ_UPD || (g.kc % 2 == 0 && g.kb % 2 == 0));
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(gemm_big_kernel<MODE, true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);

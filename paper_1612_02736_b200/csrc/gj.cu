@@ -17,6 +17,8 @@
 //
 // Work: 2 n^2 ncols flops (= (2/3)n^3 LU + (4/3)n^3 inverse + 2 n^2 (ncols-n) for the RHS),
 // all but the 2 n kb^2 per panel on DMMA tiles.
+#include <cstdlib>
+
 #include "hps_common.cuh"
 #include "hps_kernels.cuh"
 
@@ -35,7 +37,7 @@ static int gj_panel_width(int n) {
 
 // W (batch x kb x ncols doubles) followed by the inverse column permutation (batch x n ints)
 long long gj_workspace_doubles(int batch, int n, int ncols) {
-  return (long long)batch * 64 * ncols + ((long long)batch * n + 1) / 2 + 1;
+  return (long long)batch * 128 * ncols + ((long long)batch * n + 1) / 2 + 1;
 }
 
 __global__ void __launch_bounds__(GJ_THREADS) gj_panel_kernel(int n, int k0, int kb, MatB M, int* piv,
@@ -121,8 +123,8 @@ __global__ void __launch_bounds__(GJ_THREADS) gj_panel_kernel(int n, int k0, int
 // each column needs only independent loads: W[j] = M[rowid[k0+j]] and, for the displaced
 // rows outside the panel (which always receive original panel rows), M[x] = M[rowid[x]].
 // Rows inside the panel are not written: the GJ update overwrites them with panel_J W.
-__global__ void gj_swapcopy_kernel(int n, int ncols, int k0, int kb, MatB M, const int* piv, MatB W,
-                                   int batch_off) {
+__global__ void gj_swapcopy_kernel(int n, int col_lo, int col_hi, int k0, int kb, MatB M, const int* piv,
+                                   MatB W, int batch_off) {
   extern __shared__ int rowid[];  // n - k0 entries + moves
   int* moves = rowid + (n - k0);  // [0] count, then (dst, src)
   const int item = blockIdx.y + batch_off;
@@ -149,8 +151,9 @@ __global__ void gj_swapcopy_kernel(int n, int ncols, int k0, int kb, MatB M, con
   }
   __syncthreads();
   const int cl = blockIdx.x * blockDim.x + threadIdx.x;
-  if (cl >= ncols - kb) return;
-  const int c = cl < k0 ? cl : cl + kb;
+  if (cl >= (col_hi - col_lo) - kb) return;
+  int c = col_lo + cl;
+  if (c >= k0) c += kb;
   double* Mi = M.get(item);
   const long long ld = M.ld;
   double* Wi = W.get(item);
@@ -253,6 +256,93 @@ static int sm_count() {
 // outer: row interchanges + one DMMA GEMM with K = NB over all other columns).
 constexpr int GJ_OUTER_NB = 64;
 
+// Row interchanges of the panel [k0, k0+kb) applied to the columns [col_lo, col_hi) \ panel,
+// saving the pivot rows to W.
+static void swapcopy_range(int batch, int n, int col_lo, int col_hi, int k0, int kb, MatB M, const int* piv,
+                           MatB W, cudaStream_t s) {
+  const int nlog = (col_hi - col_lo) - kb;
+  if (nlog <= 0) return;
+  for (int off = 0; off < batch; off += 65535) {
+    const int bb = min(65535, batch - off);
+    dim3 g2((nlog + 127) / 128, bb);
+    gj_swapcopy_kernel<<<g2, 128, sizeof(int) * (n - k0 + 2 * kb + 4), s>>>(n, col_lo, col_hi, k0, kb, M, piv,
+                                                                            W, off);
+  }
+}
+
+// DMMA trailing update of the columns [c_lo, c_hi) by the factored panel [k0, k0+kb); the panel
+// columns are skipped when they lie inside the range.
+static int gemm_range(int batch, int n, int c_lo, int c_hi, int k0, int kb, MatB M, MatB W, cudaStream_t s) {
+  const bool inside = k0 >= c_lo && k0 < c_hi;
+  const int nlog = (c_hi - c_lo) - (inside ? kb : 0);
+  if (nlog <= 0) return 0;
+  GemmArgs g{};
+  g.M = n;
+  g.N = nlog;
+  g.K = kb;
+  g.alpha = 1.0;
+  g.beta = 1.0;
+  g.A = M;
+  g.A.off = M.off + k0;
+  g.B = W;
+  g.B.off = W.off + c_lo;
+  g.C = M;
+  g.C.off = M.off + c_lo;
+  g.k0 = k0;
+  g.kb = kb;
+  g.kc = inside ? k0 - c_lo : (1 << 30);
+  return launch_gemm(g, batch, MODE_GJ_UPD, s);
+}
+
+static int update_range(int batch, int n, int col_lo, int col_hi, int k0, int kb, MatB M, const int* piv,
+                        MatB W, cudaStream_t s) {
+  swapcopy_range(batch, n, col_lo, col_hi, k0, kb, M, piv, W, s);
+  return gemm_range(batch, n, col_lo, col_hi, k0, kb, M, W, s);
+}
+
+// Side stream + events for the look-ahead (created once, reused; stream-ordered use only).
+struct Lookahead {
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  bool ok = false;
+  Lookahead() {
+    // highest priority: the latency-bound block factorisation gets SMs first as the
+    // trailing-update GEMM's CTAs retire
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    ok = cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi) == cudaSuccess &&
+         cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming) == cudaSuccess;
+  }
+};
+
+// Factor the NB-column block starting at K0 (pivot columns [K0, K0+nb), columns of the block
+// only): one fused CTA per matrix, or for few large matrices panel-only fused launches plus
+// multi-CTA updates inside the block.
+static int factor_block(int batch, int n, int ncols, int K0, int nb, bool three_level, MatB M, int* piv,
+                        int* status, MatB W, cudaStream_t s) {
+  int rc;
+  const int kin = three_level ? gj_fused_panel_width(n, 0) : nb;
+  for (int k0 = K0; k0 < K0 + nb; k0 += kin) {
+    const int kb = min(kin, K0 + nb - k0);
+    FusedArgs f{};
+    f.batch = batch;
+    f.n = n;
+    f.ncols = ncols;
+    f.M = M;
+    f.piv = piv;
+    f.status = status;
+    f.k_begin = k0;
+    f.k_end = k0 + kb;
+    f.col_lo = three_level ? k0 : K0;
+    f.col_hi = three_level ? k0 + kb : K0 + nb;
+    f.full = 0;
+    if ((rc = launch_gj_fused(f, batch, s))) return rc;
+    if (three_level && (rc = update_range(batch, n, K0, K0 + nb, k0, kb, M, piv, W, s))) return rc;
+  }
+  return 0;
+}
+
 int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, double* anorm,
               double* ainvnorm, int* status, cudaStream_t s) {
   if (batch <= 0 || n <= 0) return 0;
@@ -280,49 +370,53 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
     int rc = launch_colnorm1(batch, n, M, anorm, s);
     if (rc) return rc;
   }
-  // equal outer blocks (multiple of 4, <= 64) so no narrow tail update is left over
-  const int nblk = (n + GJ_OUTER_NB - 1) / GJ_OUTER_NB;
+  // few large matrices: the inner level is itself split (panel-only fused kernel + multi-CTA
+  // update of the block) so the whole GPU works on each block instead of one SM per matrix
+  const bool three_level = batch * ((n + 255) / 256) < 64;
+  // equal outer blocks (multiple of 4) so no narrow tail update is left over; many matrices
+  // use K = 128 outer updates (half the read-modify-write passes over the trailing columns)
+  const int nbmax = GJ_OUTER_NB;
+  const int nblk = (n + nbmax - 1) / nbmax;
   const int NB = (((n + nblk - 1) / nblk) + 3) & ~3;
   MatB W{wbuf, (long long)NB * ncols, nullptr, ncols, 0};
+  // Look-ahead: once block K0's interchanges and the update of the NEXT block's columns are
+  // done, the next block is factored on a side stream while the main stream updates the
+  // remaining columns (disjoint column sets) — the latency-bound panel work hides under the
+  // bandwidth/compute-bound trailing GEMM.
+  static Lookahead la;
+  static int la_mode = -1;  // HPS_GJ_LOOKAHEAD: 0 never, 1 few-large only (default), 2 always
+  if (la_mode < 0) {
+    const char* e = getenv("HPS_GJ_LOOKAHEAD");
+    la_mode = e ? atoi(e) : 1;
+  }
+  const bool use_la = la.ok && (la_mode == 2 || (la_mode == 1 && three_level));
+  int rc;
+  if ((rc = factor_block(batch, n, ncols, 0, min(NB, n), three_level, M, piv, status, W, s))) return rc;
   for (int K0 = 0; K0 < n; K0 += NB) {
     const int nb = min(NB, n - K0);
-    FusedArgs f{};
-    f.batch = batch;
-    f.n = n;
-    f.ncols = ncols;
-    f.M = M;
-    f.piv = piv;
-    f.status = status;
-    f.k_begin = K0;
-    f.k_end = K0 + nb;
-    f.col_lo = K0;
-    f.col_hi = K0 + nb;
-    f.full = 0;
-    int rc = launch_gj_fused(f, batch, s);
-    if (rc) return rc;
-    if (ncols > nb) {
-      for (int off = 0; off < batch; off += 65535) {
-        const int bb = min(65535, batch - off);
-        dim3 g2((ncols - nb + 127) / 128, bb);
-        gj_swapcopy_kernel<<<g2, 128, sizeof(int) * (n - K0 + 2 * nb + 4), s>>>(n, ncols, K0, nb, M, piv, W, off);
+    const int K1 = K0 + nb;
+    const int nb1 = min(NB, n - K1);
+    swapcopy_range(batch, n, 0, ncols, K0, nb, M, piv, W, s);
+    if (nb1 > 0) {
+      if ((rc = gemm_range(batch, n, K1, K1 + nb1, K0, nb, M, W, s))) return rc;
+      if (use_la) {
+        cudaEventRecord(la.ev_a, s);
+        cudaStreamWaitEvent(la.side, la.ev_a, 0);
+        if ((rc = factor_block(batch, n, ncols, K1, nb1, three_level, M, piv, status, W, la.side))) return rc;
+        cudaEventRecord(la.ev_b, la.side);
       }
-      GemmArgs g{};
-      g.M = n;
-      g.N = ncols - nb;
-      g.K = nb;
-      g.alpha = 1.0;
-      g.beta = 1.0;
-      g.A = M;
-      g.A.off = M.off + K0;
-      g.B = W;
-      g.C = M;
-      g.k0 = K0;
-      g.kb = nb;
-      if ((rc = launch_gemm(g, batch, MODE_GJ_UPD, s))) return rc;
+    }
+    if ((rc = gemm_range(batch, n, 0, K0, K0, nb, M, W, s))) return rc;
+    if ((rc = gemm_range(batch, n, K1 + (nb1 > 0 ? nb1 : 0), ncols, K0, nb, M, W, s))) return rc;
+    if (nb1 > 0) {
+      if (use_la)
+        cudaStreamWaitEvent(s, la.ev_b, 0);
+      else if ((rc = factor_block(batch, n, ncols, K1, nb1, three_level, M, piv, status, W, s)))
+        return rc;
     }
   }
   // undo the column interchanges of the inverse block (pinv lives in the workspace after W)
-  int* pinv = reinterpret_cast<int*>(wbuf + (size_t)batch * NB * ncols);
+  int* pinv = reinterpret_cast<int*>(wbuf + (size_t)batch * 128 * ncols);
   for (int off = 0; off < batch; off += 65535) {
     const int bb = min(65535, batch - off);
     gj_perm_kernel<<<bb, 128, sizeof(int) * n, s>>>(n, piv, pinv, off);

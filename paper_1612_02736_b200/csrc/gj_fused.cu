@@ -16,6 +16,8 @@
 // Modes: full (k = 0..n over all columns, plus |A|_1, |A^-1|_1 and the final column
 // un-permutation) or sub-range (pivot columns [k_begin,k_end) updating [col_lo,col_hi)
 // only) — the inner level of the two-level blocking used for large n (gj.cu).
+#include <cstdlib>
+
 #include "hps_common.cuh"
 #include "hps_kernels.cuh"
 
@@ -33,13 +35,13 @@ __device__ __forceinline__ double block_max_nan(double v, double* red) {
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
   double m = red[0];
-  for (int w = 1; w < FU_THREADS / 32; ++w) m = (red[w] > m || red[w] != red[w]) ? red[w] : m;
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = (red[w] > m || red[w] != red[w]) ? red[w] : m;
   return m;
 }
 
 __device__ double colnorm_block(const double* Mi, long long ld, int n, double* red) {
   double best = 0.0;
-  for (int c = threadIdx.x; c < n; c += FU_THREADS) {
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int r = 0;
     for (; r + 4 <= n; r += 4) {
@@ -77,16 +79,17 @@ __device__ __forceinline__ FusedSmem carve(double* sm, int n, int ldp, int ldw) 
   s.bufA = s.W + (size_t)KB4 * ldw;
   s.bufB = s.bufA + KB4;
   s.red_v = s.bufB + KB4;
-  s.red_i = reinterpret_cast<int*>(s.red_v + 8);
-  s.spiv = s.red_i + 8;
+  s.red_i = reinterpret_cast<int*>(s.red_v + 16);
+  s.spiv = s.red_i + 24;
   s.wsrc = s.spiv + KB4;
   s.moves = s.wsrc + KB4;
   s.rowid = s.moves + 2 * KB4 + 4;
   return s;
 }
 
-template <int KB, int RPT>
-__global__ void __launch_bounds__(FU_THREADS, (RPT >= 8 ? 1 : 2)) gj_fused_kernel(FusedArgs a) {
+template <int KB, int RPT, int NTH = 256>
+__global__ void __launch_bounds__(NTH, (RPT >= 8 || NTH > 256 ? 1 : 2)) gj_fused_kernel(FusedArgs a) {
+  constexpr int FU_THREADS = NTH;
   constexpr int KB4 = (KB + 3) & ~3;
   extern __shared__ double sm[];
   const int n = a.n, ldp = a.ldp, ldw = a.ldw, CW = a.cw;
@@ -335,11 +338,11 @@ static int round_ldp(int n) { return ((n + 15) & ~15) + 4; }
 template <int KB>
 static size_t fused_smem_bytes(int n, int ldw) {
   constexpr int KB4 = (KB + 3) & ~3;
-  return sizeof(double) * ((size_t)KB4 * round_ldp(n) + (size_t)KB4 * ldw + 2 * KB4 + 8) +
-         sizeof(int) * (8 + 2 * KB4 + 2 * KB4 + 4 + (size_t)n + 4);
+  return sizeof(double) * ((size_t)KB4 * round_ldp(n) + (size_t)KB4 * ldw + 2 * KB4 + 16) +
+         sizeof(int) * (24 + 2 * KB4 + 2 * KB4 + 4 + (size_t)n + 4);
 }
 
-template <int KB, int RPT>
+template <int KB, int RPT, int NTH = 256>
 static int launch_variant(FusedArgs a, int grid, cudaStream_t s) {
   a.ldp = round_ldp(a.n);
   // chunk width: all other columns at once when they fit the budget, else 128
@@ -358,14 +361,18 @@ static int launch_variant(FusedArgs a, int grid, cudaStream_t s) {
   }
   if (smem > 227 * 1024) return 1;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(gj_fused_kernel<KB, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  gj_fused_kernel<KB, RPT><<<grid, FU_THREADS, smem, s>>>(a);
+    cudaFuncSetAttribute(gj_fused_kernel<KB, RPT, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  gj_fused_kernel<KB, RPT, NTH><<<grid, NTH, smem, s>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
 int gj_fused_panel_width(int n, int full) {
   if (full && n <= 256) return 28;
   if (n <= 512) return 16;
+  if (n <= 1024) {
+    const char* e = getenv("HPS_GJ_INNER");
+    return (e && atoi(e) == 0) ? 8 : 16;
+  }
   return 8;
 }
 
@@ -373,8 +380,16 @@ int launch_gj_fused(const FusedArgs& a, int grid, cudaStream_t s) {
   const int kb = gj_fused_panel_width(a.n, a.full);
   if (a.n <= 256 && kb == 28) return launch_variant<28, 1>(a, grid, s);
   if (a.n <= 512) return launch_variant<16, 2>(a, grid, s);
-  if (a.n <= 1024) return launch_variant<8, 4>(a, grid, s);
-  if (a.n <= 2048) return launch_variant<8, 8>(a, grid, s);
+  if (a.n <= 1024) {
+    static int v = -1;
+    if (v < 0) {
+      const char* e = getenv("HPS_GJ_INNER");
+      v = e ? atoi(e) : 1;
+    }
+    if (v == 0) return launch_variant<8, 4>(a, grid, s);
+    return launch_variant<16, 2, 512>(a, grid, s);
+  }
+  if (a.n <= 2048) return launch_variant<8, 4, 512>(a, grid, s);
   return 1;
 }
 

@@ -12,7 +12,8 @@ struct GemmArgs {
   MatB A, B, C;
   const double* bias;  // MODE_GEMM: optional M x N matrix shared by the batch, added in the epilogue
   int ldbias;
-  int k0, kb;          // MODE_GJ_UPD only
+  int k0, kb;          // MODE_GJ_UPD: pivot rows [k0, k0+kb) get beta = 0
+  int kc;              // MODE_GJ_UPD: logical column where the kb panel columns are skipped
 };
 
 int launch_gemm(const GemmArgs& g, int batch, int mode, cudaStream_t s);
