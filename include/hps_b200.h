@@ -15,6 +15,8 @@
  *   hps_gemm_batched      the dense products of solver.py:146-188 (2:1 wraps) and any batched
  *                         A.B the host needs
  *   hps_gj_invert_batched the batched FP64 pivoted inverse used by the two build steps
+ *   hps_leaf_apply        timestepping.py:117-167 the explicit side (1/k + A/2) u_n of
+ *                         Crank-Nicolson (or u_n/k for backward Euler) on every leaf
  *
  * Conventions: all matrices are row-major FP64 in DEVICE memory owned by the caller; every
  * call enqueues work on `stream` (a cudaStream_t, NULL = legacy default stream) and returns
@@ -34,7 +36,7 @@
 extern "C" {
 #endif
 
-#define HPS_ABI_VERSION 2
+#define HPS_ABI_VERSION 3
 
 enum hps_status { HPS_OK = 0, HPS_EINVAL = 1, HPS_ECUDA = 2 };
 
@@ -141,6 +143,27 @@ typedef struct {
   const int* o2idx;
 } hps_gemv_batch;
 int hps_sweep_gemv(const hps_gemv_batch* g, void* stream);
+
+/* Time-stepping right-hand side on the leaves (timestepping.py:117-167 _RhsContext.apply):
+ *   g_l[r][j] = alpha u_l[k_r][j] + beta (A u_l)[k_r][j]   at the interior nodes k_r (i_ci order),
+ * A = the collocation operator with coefficient samples coef ([6][nleaf][P]; null if beta = 0).
+ * u_l = u + l*u_stride (P rows x nrhs, x1-fastest grid), g_l = g + l*g_stride (m rows x nrhs).
+ * Crank-Nicolson: alpha = 1/k, beta = 1/2 (operator of the parabolic problem);
+ * backward Euler (config 5): alpha = 1/dt, beta = 0. */
+typedef struct {
+  int nleaf, p, nrhs;
+  double alpha, beta;
+  const double* coef;
+  const double* dx;
+  const double* dy;
+  const double* dxx;
+  const double* dyy;
+  const double* u;
+  long long u_stride;
+  double* g;
+  long long g_stride;
+} hps_leaf_apply_args;
+int hps_leaf_apply(const hps_leaf_apply_args* a, void* stream);
 
 #ifdef __cplusplus
 }

@@ -46,11 +46,18 @@ class GemvBatch(C.Structure):
                 ("a2idx", C.c_void_p), ("o2idx", C.c_void_p)]
 
 
+class LeafApplyArgs(C.Structure):
+    _fields_ = [("nleaf", C.c_int), ("p", C.c_int), ("nrhs", C.c_int), ("alpha", C.c_double),
+                ("beta", C.c_double), ("coef", C.c_void_p), ("dx", C.c_void_p), ("dy", C.c_void_p),
+                ("dxx", C.c_void_p), ("dyy", C.c_void_p), ("u", C.c_void_p), ("u_stride", C.c_longlong),
+                ("g", C.c_void_p), ("g_stride", C.c_longlong)]
+
+
 EXPORTS = ("hps_abi_version", "hps_status_string", "hps_gemm_batched", "hps_gj_workspace_bytes",
            "hps_gj_invert_batched", "hps_leaf_workspace_bytes", "hps_leaf_build",
-           "hps_merge_workspace_bytes", "hps_merge_build", "hps_sweep_gemv")
+           "hps_merge_workspace_bytes", "hps_merge_build", "hps_sweep_gemv", "hps_leaf_apply")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 _lib = None
 _lock = threading.Lock()
 
@@ -93,6 +100,7 @@ def load(build_if_missing: bool = True):
         lib.hps_merge_workspace_bytes.argtypes = [C.c_int, C.c_int, C.c_int]
         lib.hps_merge_build.argtypes = [C.POINTER(MergeBatch), C.c_void_p]
         lib.hps_sweep_gemv.argtypes = [C.POINTER(GemvBatch), C.c_void_p]
+        lib.hps_leaf_apply.argtypes = [C.POINTER(LeafApplyArgs), C.c_void_p]
         for name in EXPORTS:
             getattr(lib, name)
         if lib.hps_abi_version() != ABI_VERSION:

@@ -206,4 +206,25 @@ int hps_sweep_gemv(const hps_gemv_batch* gb, void* stream) {
   return launch_gemv_gather(a, (cudaStream_t)stream);
 }
 
+int hps_leaf_apply(const hps_leaf_apply_args* la, void* stream) {
+  if (!la || la->p < 3 || la->nrhs < 1 || !la->u || !la->g || (la->beta != 0.0 && (!la->coef || !la->dx)))
+    return HPS_EINVAL;
+  LeafApplyArgs a{};
+  a.nleaf = la->nleaf;
+  a.p = la->p;
+  a.nrhs = la->nrhs;
+  a.alpha = la->alpha;
+  a.beta = la->beta;
+  a.coef = la->coef;
+  a.dx = la->dx;
+  a.dy = la->dy;
+  a.dxx = la->dxx;
+  a.dyy = la->dyy;
+  a.u = la->u;
+  a.u_stride = la->u_stride;
+  a.g = la->g;
+  a.g_stride = la->g_stride;
+  return launch_leaf_apply(a, (cudaStream_t)stream);
+}
+
 }  // extern "C"

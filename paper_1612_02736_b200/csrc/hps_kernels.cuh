@@ -94,4 +94,20 @@ struct GemvArgs {
 };
 int launch_gemv_gather(const GemvArgs& a, cudaStream_t s);
 
+// Leaf operator application for time stepping (leaf_apply.cu)
+struct LeafApplyArgs {
+  int nleaf, p, nrhs;
+  double alpha, beta;
+  const double* coef;   // [6][nleaf][P] or null when beta == 0
+  const double* dx;
+  const double* dy;
+  const double* dxx;
+  const double* dyy;
+  const double* u;      // leaf l: u + l*u_stride, P rows x nrhs
+  long long u_stride;
+  double* g;            // leaf l: g + l*g_stride, m rows x nrhs
+  long long g_stride;
+};
+int launch_leaf_apply(const LeafApplyArgs& a, cudaStream_t s);
+
 }  // namespace hps

@@ -86,3 +86,26 @@ def config5_initial(seed: int):
 def config5_dirichlet(pts, t):
     pts = np.asarray(pts, dtype=float)
     return np.sin(2.0 * np.pi * t) * pts[:, 0] * (1.0 - pts[:, 1])
+
+
+HEAT_DECAY = 2.0 * np.pi ** 2
+
+
+def heat_problem():
+    """Manufactured heat problem u = exp(-2 pi^2 t) sin(pi x1) sin(pi x2) (reference experiments.py:302-318)."""
+    from .timestepping import ParabolicProblem
+
+    def initial(pts):
+        pts = np.asarray(pts, dtype=float)
+        return np.sin(np.pi * pts[:, 0]) * np.sin(np.pi * pts[:, 1])
+
+    def dirichlet(pts, t):
+        return np.zeros(len(pts))
+
+    return ParabolicProblem(operator=CoefficientField(-1.0, 0.0, -1.0), initial=initial,
+                            dirichlet=dirichlet, name="heat")
+
+
+def heat_exact(pts, t):
+    pts = np.asarray(pts, dtype=float)
+    return np.exp(-HEAT_DECAY * t) * np.sin(np.pi * pts[:, 0]) * np.sin(np.pi * pts[:, 1])

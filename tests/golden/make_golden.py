@@ -208,7 +208,22 @@ def solve_fixtures():
     save("cfg5_n4.npz", **a)
 
 
+def cn_fixture():
+    from specdtn.experiments import heat_problem
+    from specdtn.timestepping import TimeStepConfig, cn_run
+    tree = build_uniform_tree(UNIT, 2)
+    run = cn_run(heat_problem(), tree, TimeStepConfig(0.05, 0.2, (0.2,)), 9, 8)
+    st = run.states[0.2]
+    ids = sorted(st.leaf_solutions)
+    save("cn_heat.npz", leaf_ids=np.array(ids), leaf_sol=np.stack([st.leaf_solutions[i] for i in ids]))
+
+
 if __name__ == "__main__":
+    import sys as _sys
+    if "--only-cn" in _sys.argv:
+        cn_fixture()
+        raise SystemExit
+    cn_fixture()
     spectral_fixture()
     plan_fixture()
     leaf_fixture()
