@@ -55,9 +55,10 @@ class LeafApplyArgs(C.Structure):
 
 EXPORTS = ("hps_abi_version", "hps_status_string", "hps_gemm_batched", "hps_gj_workspace_bytes",
            "hps_gj_invert_batched", "hps_leaf_workspace_bytes", "hps_leaf_build",
-           "hps_merge_workspace_bytes", "hps_merge_build", "hps_sweep_gemv", "hps_leaf_apply")
+           "hps_merge_workspace_bytes", "hps_merge_build", "hps_sweep_gemv", "hps_leaf_apply",
+           "hps_sweep_program_bytes", "hps_sweep_program_prepare", "hps_sweep_program_run")
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 _lib = None
 _lock = threading.Lock()
 
@@ -101,6 +102,11 @@ def load(build_if_missing: bool = True):
         lib.hps_merge_build.argtypes = [C.POINTER(MergeBatch), C.c_void_p]
         lib.hps_sweep_gemv.argtypes = [C.POINTER(GemvBatch), C.c_void_p]
         lib.hps_leaf_apply.argtypes = [C.POINTER(LeafApplyArgs), C.c_void_p]
+        lib.hps_sweep_program_bytes.restype = C.c_longlong
+        lib.hps_sweep_program_bytes.argtypes = [C.c_int]
+        lib.hps_sweep_program_prepare.argtypes = [C.POINTER(GemvBatch), C.c_int, C.c_void_p,
+                                                  C.POINTER(C.c_longlong)]
+        lib.hps_sweep_program_run.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_longlong, C.c_void_p]
         for name in EXPORTS:
             getattr(lib, name)
         if lib.hps_abi_version() != ABI_VERSION:

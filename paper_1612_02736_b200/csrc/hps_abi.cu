@@ -179,6 +179,61 @@ int hps_merge_build(const hps_merge_batch* Mb, void* stream) {
   return launch_gemm(g, np, MODE_GEMM, s);
 }
 
+static int to_gemv_args(const hps_gemv_batch* gb, GemvArgs* out) {
+  if (!gb || !gb->pool || !gb->xidx || !gb->oidx || gb->nrhs < 1 || gb->nrhs > 16) return HPS_EINVAL;
+  GemvArgs a{};
+  a.nitems = gb->nitems;
+  a.R = gb->R;
+  a.K = gb->K;
+  a.nrhs = gb->nrhs;
+  a.A = to_matb(&gb->A);
+  a.pool = gb->pool;
+  a.xidx = gb->xidx;
+  a.x2idx = gb->x2idx;
+  a.aidx = gb->aidx;
+  a.oidx = gb->oidx;
+  a.mode2 = gb->mode2;
+  a.R2 = gb->R2;
+  a.K2 = gb->K2;
+  a.A2 = to_matb(&gb->A2);
+  a.a2idx = gb->a2idx;
+  a.o2idx = gb->o2idx;
+  a.xstride = a.K;
+  a.ostride = a.R;
+  if (a.mode2 && (!a.o2idx || a.R2 <= 0 || a.K2 <= 0 || (a.mode2 == 1 && a.K2 > a.K) ||
+                  (a.mode2 == 2 && a.K2 != a.R) || a.mode2 > 2))
+    return HPS_EINVAL;
+  *out = a;
+  return HPS_OK;
+}
+
+long long hps_sweep_program_bytes(int nsteps) { return (long long)sizeof(SweepStep) * (nsteps > 0 ? nsteps : 0); }
+
+int hps_sweep_program_prepare(const hps_gemv_batch* steps, int nsteps, void* dev_buffer, long long* smem_bytes) {
+  if (!steps || nsteps <= 0 || !dev_buffer || !smem_bytes) return HPS_EINVAL;
+  GemvArgs* ga = new GemvArgs[nsteps];
+  SweepStep* ss = new SweepStep[nsteps];
+  int rc = HPS_OK;
+  for (int i = 0; i < nsteps && rc == HPS_OK; ++i) {
+    rc = to_gemv_args(&steps[i], &ga[i]);
+    if (rc == HPS_OK && ga[i].nrhs != ga[0].nrhs) rc = HPS_EINVAL;
+  }
+  if (rc == HPS_OK) {
+    sweep_program_fill(ga, nsteps, ss);
+    *smem_bytes = (long long)sweep_program_smem(ga, nsteps, ga[0].nrhs <= 1 ? 1 : 2);
+    if (cudaMemcpy(dev_buffer, ss, sizeof(SweepStep) * nsteps, cudaMemcpyHostToDevice) != cudaSuccess) rc = HPS_ECUDA;
+  }
+  delete[] ga;
+  delete[] ss;
+  return rc;
+}
+
+int hps_sweep_program_run(const void* dev_buffer, int nsteps, int nrhs, long long smem_bytes, void* stream) {
+  if (!dev_buffer || nsteps <= 0 || nrhs < 1 || nrhs > 2) return HPS_EINVAL;
+  return launch_sweep_program((const SweepStep*)dev_buffer, nsteps, nrhs, (size_t)smem_bytes,
+                              (cudaStream_t)stream);
+}
+
 int hps_sweep_gemv(const hps_gemv_batch* gb, void* stream) {
   if (!gb || !gb->pool || !gb->xidx || !gb->oidx || gb->nrhs < 1 || gb->nrhs > 16) return HPS_EINVAL;
   GemvArgs a{};

@@ -10,8 +10,12 @@
 // Bandwidth-bound: each operator entry is read once per call and used for nrhs FMAs.
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "hps_common.cuh"
 #include "hps_kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace hps {
 
@@ -360,26 +364,25 @@ __device__ __forceinline__ void rows_dot(const double* __restrict__ A, long long
 
 __host__ __device__ inline int lanes_for(int K) { return K <= 16 ? 4 : (K <= 48 ? 8 : (K <= 128 ? 16 : 32)); }
 
+// One work unit of a sweep step: item `item`, row chunk `chunk` of `nchunks` (rows_per_cta rows).
 template <int NR, bool VEC, int RB = 2, int U = 4>
-__global__ void __launch_bounds__(256) sweep_kernel(GemvArgs a, int rows_per_cta, int batch_off) {
-  extern __shared__ double sm[];
+__device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chunk, int nchunks, int rows_per_cta,
+                                           double* sm) {
   double* xs = sm;                        // K x NR
   double* ys = xs + (size_t)a.K * NR;     // R x NR (chain mode)
-  const int item = blockIdx.y + batch_off;
   const int K = a.K, nrhs = a.nrhs;
   const int* xi = a.xidx + (long long)item * a.xstride;
   const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
   const double* pool = a.pool;
-  {
-    // start streaming this CTA's operator rows into L2 while x is gathered
-    const int p0 = blockIdx.x * rows_per_cta, p1 = min(a.R, p0 + rows_per_cta);
-    const double* Ai = a.A.get(item);
-    for (int r = p0 + threadIdx.x; r < p1; r += blockDim.x) {
-      const double* rp = Ai + (long long)r * a.A.ld;
-      const uintptr_t lo = reinterpret_cast<uintptr_t>(rp) & ~(uintptr_t)15;
-      const uintptr_t hi = (reinterpret_cast<uintptr_t>(rp + K) + 15) & ~(uintptr_t)15;
-      prefetch_l2_bulk(reinterpret_cast<const void*>(lo), (unsigned)(hi - lo));
-    }
+  const double* Ai = a.A.get(item);
+  const int r0 = chunk * rows_per_cta;
+  const int r1 = min(a.R, r0 + rows_per_cta);
+  // start streaming this unit's operator rows into L2 while x is gathered
+  for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    const double* rp = Ai + (long long)r * a.A.ld;
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(rp) & ~(uintptr_t)15;
+    const uintptr_t hi = (reinterpret_cast<uintptr_t>(rp + K) + 15) & ~(uintptr_t)15;
+    prefetch_l2_bulk(reinterpret_cast<const void*>(lo), (unsigned)(hi - lo));
   }
   for (int e = threadIdx.x; e < K * NR; e += blockDim.x) {
     const int k = e / NR, j = e - k * NR;
@@ -391,24 +394,47 @@ __global__ void __launch_bounds__(256) sweep_kernel(GemvArgs a, int rows_per_cta
     xs[e] = v;
   }
   __syncthreads();
-  const int r0 = blockIdx.x * rows_per_cta;
-  const int r1 = min(a.R, r0 + rows_per_cta);
-  rows_dot<NR, VEC, RB, U>(a.A.get(item), a.A.ld, a.R, r0, r1, K, lanes_for(K), xs,
-               a.aidx ? a.aidx + (long long)item * a.ostride : nullptr, a.oidx + (long long)item * a.ostride,
-               a.pool, nrhs, a.mode2 == 2 ? ys : nullptr);
+  rows_dot<NR, VEC, RB, U>(Ai, a.A.ld, a.R, r0, r1, K, lanes_for(K), xs,
+                           a.aidx ? a.aidx + (long long)item * a.ostride : nullptr,
+                           a.oidx + (long long)item * a.ostride, a.pool, nrhs, a.mode2 == 2 ? ys : nullptr);
   if (a.mode2 == 1) {
     // tail stage rows split evenly over the row chunks of this item
-    const int per = (a.R2 + gridDim.x - 1) / gridDim.x;
-    const int s0 = blockIdx.x * per, s1 = min(a.R2, s0 + per);
+    const int per = (a.R2 + nchunks - 1) / nchunks;
+    const int s0 = chunk * per, s1 = min(a.R2, s0 + per);
     rows_dot<NR, false>(a.A2.get(item), a.A2.ld, a.R2, s0, s1, a.K2, lanes_for(a.K2), xs + (size_t)(K - a.K2) * NR,
-                 a.a2idx ? a.a2idx + (long long)item * a.R2 : nullptr, a.o2idx + (long long)item * a.R2, a.pool,
-                 nrhs, nullptr);
+                        a.a2idx ? a.a2idx + (long long)item * a.R2 : nullptr, a.o2idx + (long long)item * a.R2,
+                        a.pool, nrhs, nullptr);
   } else if (a.mode2 == 2) {
     __syncthreads();
-    const double* x2s = ys;
-    rows_dot<NR, false>(a.A2.get(item), a.A2.ld, a.R2, 0, a.R2, a.K2, lanes_for(a.K2), x2s,
-                 a.a2idx ? a.a2idx + (long long)item * a.R2 : nullptr, a.o2idx + (long long)item * a.R2, a.pool,
-                 nrhs, nullptr);
+    rows_dot<NR, false>(a.A2.get(item), a.A2.ld, a.R2, 0, a.R2, a.K2, lanes_for(a.K2), ys,
+                        a.a2idx ? a.a2idx + (long long)item * a.R2 : nullptr, a.o2idx + (long long)item * a.R2,
+                        a.pool, nrhs, nullptr);
+  }
+}
+
+template <int NR, bool VEC, int RB = 2, int U = 4>
+__global__ void __launch_bounds__(256) sweep_kernel(GemvArgs a, int rows_per_cta, int batch_off) {
+  extern __shared__ double sm[];
+  sweep_unit<NR, VEC, RB, U>(a, blockIdx.y + batch_off, blockIdx.x, gridDim.x, rows_per_cta, sm);
+}
+
+// Whole solve program in one cooperative launch: the steps run in order, separated by a
+// grid-wide barrier; the work units of a step (item x row chunk) are dealt round-robin over
+// the resident CTAs. Removes the per-level launch latency of the ~30 short tree levels.
+template <int NR>
+__global__ void __launch_bounds__(256) sweep_mega_kernel(const SweepStep* steps, int nsteps) {
+  extern __shared__ double sm[];
+  cg::grid_group grid = cg::this_grid();
+  for (int s = 0; s < nsteps; ++s) {
+    const GemvArgs a = steps[s].a;
+    const int nch = steps[s].nchunks, rows = steps[s].rows_per_cta;
+    const int units = a.nitems * nch;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int item = u / nch;
+      sweep_unit<NR, false>(a, item, u - item * nch, nch, rows, sm);
+      __syncthreads();
+    }
+    grid.sync();
   }
 }
 
@@ -457,6 +483,49 @@ static void launch_dmma(const GemvArgs& a, cudaStream_t s) {
   }
 }
 
+static int sweep_rows_per_cta(const GemvArgs& a) {
+  int rows = a.R;
+  if (a.mode2 != 2) {
+    const int G = 32 / lanes_for(a.K);
+    const int minrows = 8 * G * 2;
+    rows = a.R < 64 ? a.R : 64;
+    while (rows > minrows && (long long)a.nitems * ((a.R + rows - 1) / rows) < 4 * 148) rows = (rows + 1) / 2;
+    if (rows < minrows) rows = minrows < a.R ? minrows : a.R;
+  }
+  return rows;
+}
+
+size_t sweep_program_smem(const GemvArgs* steps, int n, int nr) {
+  size_t m = 0;
+  for (int i = 0; i < n; ++i) {
+    const size_t b = sizeof(double) * nr * ((size_t)steps[i].K + (steps[i].mode2 == 2 ? steps[i].R : 0));
+    if (b > m) m = b;
+  }
+  return m;
+}
+
+void sweep_program_fill(const GemvArgs* steps, int n, SweepStep* out) {
+  for (int i = 0; i < n; ++i) {
+    out[i].a = steps[i];
+    out[i].rows_per_cta = sweep_rows_per_cta(steps[i]);
+    out[i].nchunks = (steps[i].R + out[i].rows_per_cta - 1) / out[i].rows_per_cta;
+  }
+}
+
+int launch_sweep_program(const SweepStep* dsteps, int n, int nrhs, size_t smem, cudaStream_t s) {
+  if (nrhs > 2 || smem > 48 * 1024) return 1;
+  void* fn = nrhs == 1 ? (void*)sweep_mega_kernel<1> : (void*)sweep_mega_kernel<2>;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
+  if (per_sm <= 0) return 1;
+  const int grid = per_sm * sms;
+  void* args[] = {(void*)&dsteps, (void*)&n};
+  const cudaError_t err = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, smem, s);
+  return err == cudaSuccess ? 0 : 2;
+}
+
 template <int NR>
 static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
   {
@@ -469,14 +538,7 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
   }
   const size_t smem = sizeof(double) * NR * ((size_t)a.K + (a.mode2 == 2 ? a.R : 0));
   if (smem > 48 * 1024) return false;
-  int rows = a.R;
-  if (a.mode2 != 2) {
-    const int G = 32 / lanes_for(a.K);
-    const int minrows = 8 * G * 2;
-    rows = a.R < 64 ? a.R : 64;
-    while (rows > minrows && (long long)a.nitems * ((a.R + rows - 1) / rows) < 4 * 148) rows = (rows + 1) / 2;
-    if (rows < minrows) rows = minrows < a.R ? minrows : a.R;
-  }
+  const int rows = sweep_rows_per_cta(a);
   const int gx = (a.R + rows - 1) / rows;
   static int variant = -1;
   if (variant < 0) {

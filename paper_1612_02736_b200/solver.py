@@ -290,13 +290,25 @@ class FactorizedSolver:
         N = self.plan.n_gauss
         s = _stream_ptr()
         pool[:2 * N].zero_()
+        mega = prog["mega"].get("full" if down else "up")
+        if mega is not None:
+            ng = len(self.leaf_groups)
+            buf, n, smem = mega
+            for step in prog["up"][:ng]:
+                _ext.check(lib.hps_sweep_gemv(step, s), "upward sweep")
+            _ext.check(lib.hps_sweep_program_run(buf.data_ptr(), n, pool.shape[1], smem, s), "sweep program")
+            if down:
+                for step in prog["down"][-ng:]:
+                    _ext.check(lib.hps_sweep_gemv(step, s), "downward sweep")
+            return
         for step in prog["up"]:
             _ext.check(lib.hps_sweep_gemv(step, s), "upward sweep")
         if not down:
             return
-        pool.index_copy_(0, prog["root_rows"], prog["f_in"])
         for step in prog["down"]:
             _ext.check(lib.hps_sweep_gemv(step, s), "downward sweep")
+
+    use_mega = False  # single cooperative launch for the parent levels (hps_sweep_program_run); measured slower than graph replay on B200 (r01), opt-in
 
     def _execute(self, prog, down=True):
         if self.mode == "econ":
@@ -419,15 +431,18 @@ class FactorizedSolver:
         def split(spec):
             if spec["mode2"] or spec["K"] < 512:
                 return [spec]
-            if nrhs <= 2 and 8 * spec["nitems"] * spec["R"] * spec["K"] < 64e6:
-                return [spec]  # single-RHS: the extra reduction launch costs more than it saves
+            K = spec["K"]
+            # the single-launch sweep program stages each step's x in 48 KB of shared memory
+            must = nrhs <= 2 and K * 8 * nrhs > 40 * 1024
+            if not must and nrhs <= 2 and 8 * spec["nitems"] * spec["R"] * K < 64e6:
+                return [spec]  # single-RHS: the extra reduction step costs more than it saves
             rows_min = 16 if nrhs > 2 else 8
             ctas = spec["nitems"] * -(-spec["R"] // rows_min)
-            if ctas >= 600:
+            if ctas >= 600 and not must:
                 return [spec]
-            K = spec["K"]
-            want = min(-(-600 // ctas), K // 128)
-            ns = max([d for d in range(1, want + 1) if K % d == 0] or [1])
+            want = max(min(-(-600 // ctas), K // 128), -(-K * 8 * nrhs // (40 * 1024)) if must else 1)
+            ns = min([d for d in range(want, K + 1) if K % d == 0] or [1]) if must else \
+                max([d for d in range(1, want + 1) if K % d == 0] or [1])
             if ns <= 1:
                 return [spec]
             kc = K // ns
@@ -457,6 +472,16 @@ class FactorizedSolver:
 
         up = [s2 for s1 in up for s2 in split(s1)]
         down = [s2 for s1 in down for s2 in split(s1)]
+        # Dirichlet data: rows F of the pool, copied onto the root exterior by a 1x1 "gemv" step
+        root_ext = plan.node[tree.root].ext
+        f_rows = scratch[0]
+        scratch[0] += root_ext.size
+        one = torch.ones(1, dtype=torch.float64, device=self.device)
+        keep.append(one)
+        copy_f = dict(nitems=root_ext.size, R=1, K=1, A=_ext.mat(one, 0, 1),
+                      xidx=(f_rows + np.arange(root_ext.size))[:, None], oidx=(lay["U"] + root_ext)[:, None],
+                      x2idx=None, aidx=None, mode2=0, R2=0, K2=0, A2=None, o2idx=None, a2idx=None)
+        down = [copy_f] + down
         pool = torch.zeros((scratch[0], nrhs), dtype=torch.float64, device=self.device)
 
         def build(spec):
@@ -474,9 +499,21 @@ class FactorizedSolver:
                    for i, s_ in enumerate(lst) if "patch" in s_]
         up = [build(s_) for s_ in up]
         down = [build(s_) for s_ in down]
-        root_rows = torch.as_tensor(lay["U"] + plan.node[tree.root].ext, dtype=torch.long, device=self.device)
-        f_in = torch.zeros((root_rows.numel(), nrhs), dtype=torch.float64, device=self.device)
-        prog = {"pool": pool, "up": up, "down": down, "keep": keep, "root_rows": root_rows, "f_in": f_in,
+        f_in = pool[f_rows:f_rows + root_ext.size]
+        mega = {}
+        ng = len(self.leaf_groups)
+        if nrhs <= 2 and self.mode != "econ" and self.use_mega and len(up) > ng:
+            # the latency-bound middle (parent levels + the f copy) runs as ONE cooperative
+            # launch; the bandwidth-bound leaf steps keep their own full-occupancy launches
+            lib = _ext.load()
+            for name, steps in (("full", up[ng:] + down[:-ng]), ("up", up[ng:])):
+                arr = (_ext.GemvBatch * len(steps))(*steps)
+                buf = torch.empty(int(lib.hps_sweep_program_bytes(len(steps))), dtype=torch.uint8, device=self.device)
+                smem = _ext.C.c_longlong(0)
+                rc = lib.hps_sweep_program_prepare(arr, len(steps), buf.data_ptr(), _ext.C.byref(smem))
+                if rc == 0 and smem.value <= 48 * 1024:
+                    mega[name] = (buf, len(steps), smem.value)
+        prog = {"pool": pool, "up": up, "down": down, "keep": keep, "f_in": f_in, "mega": mega,
                 "graph": None, "patches": patches}
         self._sweeps[nrhs] = prog
         return prog

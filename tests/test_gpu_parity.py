@@ -197,3 +197,17 @@ class TestEconomyMode:
     def test_unknown_mode(self):
         with pytest.raises(ValueError, match="unknown mode"):
             build_stage(build_uniform_tree(UNIT, 1), catalog("laplace"), 9, 8, mode="compressed")
+
+
+def test_cooperative_sweep_program_matches_graph_path():
+    spec = catalog("varcoef_helmholtz", kappa=10.0)
+    tree = build_uniform_tree(UNIT, 8)
+    a = build_stage(tree, spec, 12, 11)
+    b = build_stage(tree, spec, 12, 11)
+    b.use_mega = True
+    f = lambda pts: np.sin(2 * pts[:, 0] + pts[:, 1])
+    sa, sb = a.solve(f=f), b.solve(f=f)
+    assert b._program(1)["mega"], "cooperative program was not prepared"
+    assert rel_maxdiff(sb.u, sa.u) <= 1e-14
+    for nid in sa.leaf_solutions:
+        np.testing.assert_allclose(sb.leaf_solutions[nid], sa.leaf_solutions[nid], rtol=0, atol=1e-13)
