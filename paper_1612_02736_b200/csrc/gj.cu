@@ -25,6 +25,9 @@
 namespace hps {
 
 constexpr int GJ_THREADS = 256;
+// Outer block width of the two-level scheme (inner: fused kernel on the NB-column block;
+// outer: row interchanges + one DMMA GEMM with K = NB over all other columns).
+constexpr int GJ_OUTER_NB = 64;
 constexpr int GJ_SMEM_BUDGET = 220 * 1024;
 
 static int gj_panel_width(int n) {
@@ -36,8 +39,12 @@ static int gj_panel_width(int n) {
 }
 
 // W (batch x kb x ncols doubles) followed by the inverse column permutation (batch x n ints)
+static int sm_count();
+static bool gj_is_fused_full(int batch, int n) { return n <= 256 && (batch >= sm_count() || n <= 64); }
+
 long long gj_workspace_doubles(int batch, int n, int ncols) {
-  return (long long)batch * 128 * ncols + ((long long)batch * n + 1) / 2 + 1;
+  if (gj_is_fused_full(batch, n)) return 1;  // the fused kernel needs no global workspace
+  return (long long)batch * GJ_OUTER_NB * ncols + ((long long)batch * n + 1) / 2 + 1;
 }
 
 __global__ void __launch_bounds__(GJ_THREADS) gj_panel_kernel(int n, int k0, int kb, MatB M, int* piv,
@@ -252,9 +259,6 @@ static int sm_count() {
   return sms;
 }
 
-// Outer block width of the two-level scheme (inner: fused kernel on the NB-column block;
-// outer: row interchanges + one DMMA GEMM with K = NB over all other columns).
-constexpr int GJ_OUTER_NB = 64;
 
 // Row interchanges of the panel [k0, k0+kb) applied to the columns [col_lo, col_hi) \ panel,
 // saving the pivot rows to W.
@@ -347,7 +351,7 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
               double* ainvnorm, int* status, cudaStream_t s) {
   if (batch <= 0 || n <= 0) return 0;
   const int sms = sm_count();
-  const bool fused_full = n <= 256 && (batch >= sms || n <= 64);
+  const bool fused_full = gj_is_fused_full(batch, n);
   if (fused_full) {
     FusedArgs f{};
     f.batch = batch;
@@ -416,7 +420,7 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
     }
   }
   // undo the column interchanges of the inverse block (pinv lives in the workspace after W)
-  int* pinv = reinterpret_cast<int*>(wbuf + (size_t)batch * 128 * ncols);
+  int* pinv = reinterpret_cast<int*>(wbuf + (size_t)batch * GJ_OUTER_NB * ncols);
   for (int off = 0; off < batch; off += 65535) {
     const int bb = min(65535, batch - off);
     gj_perm_kernel<<<bb, 128, sizeof(int) * n, s>>>(n, piv, pinv, off);

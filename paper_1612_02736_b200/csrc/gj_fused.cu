@@ -60,8 +60,8 @@ __device__ double colnorm_block(const double* Mi, long long ld, int n, double* r
 struct FusedSmem {
   double* P;
   double* W;
-  double* bufA;
-  double* bufB;
+  double* slots;  // [2][warps][KB+2]: candidate value, row index, row values
+  double* bufB;   // [2][KB]: displaced row
   double* red_v;
   int* red_i;
   int* spiv;
@@ -76,9 +76,9 @@ __device__ __forceinline__ FusedSmem carve(double* sm, int n, int ldp, int ldw) 
   FusedSmem s;
   s.P = sm;
   s.W = s.P + (size_t)KB4 * ldp;
-  s.bufA = s.W + (size_t)KB4 * ldw;
-  s.bufB = s.bufA + KB4;
-  s.red_v = s.bufB + KB4;
+  s.slots = s.W + (size_t)KB4 * ldw;
+  s.bufB = s.slots + 2 * 16 * (KB + 2);
+  s.red_v = s.bufB + 2 * KB4;
   s.red_i = reinterpret_cast<int*>(s.red_v + 16);
   s.spiv = s.red_i + 24;
   s.wsrc = s.spiv + KB4;
@@ -119,71 +119,94 @@ __global__ void __launch_bounds__(NTH, (RPT >= 8 || NTH > 256 ? 1 : 2)) gj_fused
 #pragma unroll
         for (int t = 0; t < KB; ++t) row[r][t] = (i < n && t < kbc) ? src[t] : 0.0;
       }
-#pragma unroll
+      // Column loop with the panel row rotated in registers so the current column is always
+      // row[.][0] (the loop body has static register indices and is NOT unrolled: 1/KB the code
+      // of a fully unrolled loop, no instruction-cache thrash). One barrier per column: every
+      // warp publishes its best candidate row (double-buffered slots), every thread then picks
+      // the global winner (LAPACK rule: largest |value|, ties -> smallest row) itself.
+#pragma unroll 1
       for (int j = 0; j < KB; ++j) {
-        if (j >= kbc) break;
-        const int cj = k0 + j;
-        double best = -1.0;
-        int bi = n;
+        if (j < kbc) {
+          const int cj = k0 + j;
+          double* slots = S.slots + (j & 1) * (FU_THREADS / 32) * (KB + 2);
+          double* disp = S.bufB + (j & 1) * KB;
+          double best = -1.0;
+          int bi = n;
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const int i = tid + r * FU_THREADS;
+            if (i < n && i >= cj) {
+              const double v = fabs(row[r][0]);
+              if (v > best) { best = v; bi = i; }
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+          }
+          double* my = slots + warp * (KB + 2);
+          if (lane == 0) {
+            my[0] = best;
+            my[1] = (double)bi;
+          }
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const int i = tid + r * FU_THREADS;
+            if (i == bi) {
+#pragma unroll
+              for (int t = 0; t < KB; ++t) my[2 + t] = row[r][t];
+            }
+            if (i == cj) {
+#pragma unroll
+              for (int t = 0; t < KB; ++t) disp[t] = row[r][t];
+            }
+          }
+          __syncthreads();
+          double b = slots[0];
+          int pr = (int)slots[1], ws = 0;
+#pragma unroll
+          for (int w = 1; w < FU_THREADS / 32; ++w) {
+            const double vw = slots[w * (KB + 2)];
+            const int iw = (int)slots[w * (KB + 2) + 1];
+            if (vw > b || (vw == b && iw < pr)) { b = vw; pr = iw; ws = w; }
+          }
+          const double* pvr = slots + ws * (KB + 2) + 2;
+          if (pr >= n) {  // all candidates NaN: keep the diagonal, NaN propagates
+            pr = cj;
+            pvr = disp;
+          }
+          if (tid == 0) {
+            if (!(b > 0.0)) flag = 1;
+            S.spiv[j] = pr;
+            piv[cj] = pr;
+          }
+          const double inv = 1.0 / pvr[0];
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const int i = tid + r * FU_THREADS;
+            if (i == pr && pr != cj) {
+#pragma unroll
+              for (int t = 0; t < KB; ++t) row[r][t] = disp[t];
+            }
+            if (i == cj) {
+#pragma unroll
+              for (int t = 0; t < KB; ++t) row[r][t] = (t == 0) ? inv : pvr[t] * inv;
+            } else {
+              const double f = row[r][0];
+#pragma unroll
+              for (int t = 0; t < KB; ++t) row[r][t] = ((t == 0) ? 0.0 : row[r][t]) - f * ((t == 0) ? inv : pvr[t] * inv);
+            }
+          }
+        }
+        // rotate: next column to the front (KB rotations in total restore the column order)
 #pragma unroll
         for (int r = 0; r < RPT; ++r) {
-          const int i = tid + r * FU_THREADS;
-          if (i < n && i >= cj) {
-            const double v = fabs(row[r][j]);
-            if (v > best) { best = v; bi = i; }
-          }
-        }
+          const double t0 = row[r][0];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-        }
-        if (lane == 0) { S.red_v[warp] = best; S.red_i[warp] = bi; }
-        __syncthreads();
-        double b = S.red_v[0];
-        int pr = S.red_i[0];
-#pragma unroll
-        for (int w = 1; w < FU_THREADS / 32; ++w) {
-          const double vw = S.red_v[w];
-          const int iw = S.red_i[w];
-          if (vw > b || (vw == b && iw < pr)) { b = vw; pr = iw; }
-        }
-        if (pr >= n) pr = cj;
-        if (tid == 0) {
-          if (!(b > 0.0)) flag = 1;
-          S.spiv[j] = pr;
-          piv[cj] = pr;
-        }
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-          const int i = tid + r * FU_THREADS;
-          if (i == pr) {
-#pragma unroll
-            for (int t = 0; t < KB; ++t) S.bufA[t] = row[r][t];
-          }
-          if (i == cj && pr != cj) {
-#pragma unroll
-            for (int t = 0; t < KB; ++t) S.bufB[t] = row[r][t];
-          }
-        }
-        __syncthreads();
-        const double inv = 1.0 / S.bufA[j];
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-          const int i = tid + r * FU_THREADS;
-          if (i == pr && pr != cj) {
-#pragma unroll
-            for (int t = 0; t < KB; ++t) row[r][t] = S.bufB[t];
-          }
-          if (i == cj) {
-#pragma unroll
-            for (int t = 0; t < KB; ++t) row[r][t] = (t == j) ? inv : S.bufA[t] * inv;
-          } else {
-            const double f = row[r][j];
-#pragma unroll
-            for (int t = 0; t < KB; ++t) row[r][t] = ((t == j) ? 0.0 : row[r][t]) - f * ((t == j) ? inv : S.bufA[t] * inv);
-          }
+          for (int t = 0; t < KB - 1; ++t) row[r][t] = row[r][t + 1];
+          row[r][KB - 1] = t0;
         }
       }
 
@@ -338,7 +361,7 @@ static int round_ldp(int n) { return ((n + 15) & ~15) + 4; }
 template <int KB>
 static size_t fused_smem_bytes(int n, int ldw) {
   constexpr int KB4 = (KB + 3) & ~3;
-  return sizeof(double) * ((size_t)KB4 * round_ldp(n) + (size_t)KB4 * ldw + 2 * KB4 + 16) +
+  return sizeof(double) * ((size_t)KB4 * round_ldp(n) + (size_t)KB4 * ldw + 2 * 16 * (KB + 2) + 2 * KB4 + 16) +
          sizeof(int) * (24 + 2 * KB4 + 2 * KB4 + 4 + (size_t)n + 4);
 }
 
