@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define HPS_ABI_VERSION 4
+#define HPS_ABI_VERSION 5
 
 enum hps_status { HPS_OK = 0, HPS_EINVAL = 1, HPS_ECUDA = 2 };
 
@@ -60,11 +60,14 @@ int hps_gemm_batched(int batch, int M, int N, int K, double alpha, const hps_mat
 
 /* In-place inverse of the leading n x n block of M_i (n x ncols); trailing columns become
  * inv(A_i) * rhs_i. piv: batch*n ints; workspace: hps_gj_workspace_bytes; anorm / ainvnorm
- * (nullable): 1-norms of A_i and inv(A_i); status (nullable): per-item flags. */
+ * (nullable): 1-norms of A_i and inv(A_i); status (nullable): per-item flags.
+ * perm (nullable, batch*n ints): if given, the inverse's columns are left in pivot order,
+ * M_i[:, j] = inv(A_i)[:, perm_i[j]] (so inv(A_i) b = M_i[:, :n] b[perm_i]) and perm is
+ * written — saves the un-permutation pass; else the columns are restored. */
 long long hps_gj_workspace_bytes(int batch, int n, int ncols);
 int hps_gj_invert_batched(int batch, int n, int ncols, const hps_mat_batch* M, int* piv,
                           void* workspace, double* anorm, double* ainvnorm, int* status,
-                          void* stream);
+                          int* perm, void* stream);
 
 /* Leaf stage for `nleaf` leaves of one shape (p Chebyshev nodes per side, q Gauss nodes per
  * edge; m = (p-2)^2 interior, b = 4q Gauss, c = 4(p-1) exterior Chebyshev, P = p^2).
@@ -91,6 +94,8 @@ typedef struct {
   double* anorm;
   double* ainvnorm;
   int* status;
+  int* perm;            /* nullable: F_ii left in pivot column order, perm (nleaf x m) written
+                           (see hps_gj_invert_batched); H then shares the same column order */
   void* workspace;      /* hps_leaf_workspace_bytes */
 } hps_leaf_batch;
 long long hps_leaf_workspace_bytes(int nleaf, int p, int q);
@@ -117,6 +122,7 @@ typedef struct {
   double* dnorm;
   double* xnorm;
   int* status;
+  int* perm;            /* nullable: X left in pivot column order, perm (npar x m3) written */
   void* workspace;      /* hps_merge_workspace_bytes */
 } hps_merge_batch;
 long long hps_merge_workspace_bytes(int npar, int m3, int e);

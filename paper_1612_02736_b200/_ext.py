@@ -27,7 +27,7 @@ class LeafBatch(C.Structure):
                 ("ext_pos", C.c_void_p), ("lift", C.c_void_p), ("dfi", C.c_void_p),
                 ("t0", C.c_void_p), ("fs", C.c_void_p), ("h", C.c_void_p), ("t", C.c_void_p),
                 ("anorm", C.c_void_p), ("ainvnorm", C.c_void_p), ("status", C.c_void_p),
-                ("workspace", C.c_void_p)]
+                ("perm", C.c_void_p), ("workspace", C.c_void_p)]
 
 
 class MergeBatch(C.Structure):
@@ -35,7 +35,8 @@ class MergeBatch(C.Structure):
                 ("ta", C.c_void_p), ("tb", C.c_void_p), ("lda", C.c_int), ("ldb", C.c_int),
                 ("idx", C.c_void_p), ("idx_stride", C.c_longlong), ("xs", C.c_void_p),
                 ("tei", C.c_void_p), ("tnew", C.c_void_p), ("dnorm", C.c_void_p),
-                ("xnorm", C.c_void_p), ("status", C.c_void_p), ("workspace", C.c_void_p)]
+                ("xnorm", C.c_void_p), ("status", C.c_void_p), ("perm", C.c_void_p),
+                ("workspace", C.c_void_p)]
 
 
 class GemvBatch(C.Structure):
@@ -58,7 +59,7 @@ EXPORTS = ("hps_abi_version", "hps_status_string", "hps_gemm_batched", "hps_gj_w
            "hps_merge_workspace_bytes", "hps_merge_build", "hps_sweep_gemv", "hps_leaf_apply",
            "hps_sweep_program_bytes", "hps_sweep_program_prepare", "hps_sweep_program_run")
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 _lib = None
 _lock = threading.Lock()
 
@@ -93,7 +94,7 @@ def load(build_if_missing: bool = True):
         lib.hps_gj_workspace_bytes.argtypes = [C.c_int, C.c_int, C.c_int]
         lib.hps_gj_invert_batched.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(MatBatch),
                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                              C.c_void_p, C.c_void_p]
+                                              C.c_void_p, C.c_void_p, C.c_void_p]
         lib.hps_leaf_workspace_bytes.restype = C.c_longlong
         lib.hps_leaf_workspace_bytes.argtypes = [C.c_int, C.c_int, C.c_int]
         lib.hps_leaf_build.argtypes = [C.POINTER(LeafBatch), C.c_void_p]

@@ -173,8 +173,9 @@ __global__ void gj_swapcopy_kernel(int n, int col_lo, int col_hi, int k0, int kb
   }
 }
 
-// inverse column permutation pinv (pinv[perm[j]] = j) from the LAPACK interchange list
-__global__ void gj_perm_kernel(int n, const int* piv, int* pinv, int batch_off) {
+// inverse column permutation pinv (pinv[perm[j]] = j) from the LAPACK interchange list, or
+// perm itself when want_perm
+__global__ void gj_perm_kernel(int n, const int* piv, int* pinv, int batch_off, int want_perm) {
   extern __shared__ int perm[];
   const int item = blockIdx.x + batch_off;
   const int* pv = piv + (long long)item * n;
@@ -190,7 +191,12 @@ __global__ void gj_perm_kernel(int n, const int* piv, int* pinv, int batch_off) 
   }
   __syncthreads();
   int* out = pinv + (long long)item * n;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) out[perm[j]] = j;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    if (want_perm)
+      out[j] = perm[j];
+    else
+      out[perm[j]] = j;
+  }
 }
 
 // F[r][c] = M[r][pinv[c]] for c < n, one warp per row, row staged in shared memory
@@ -348,7 +354,7 @@ static int factor_block(int batch, int n, int ncols, int K0, int nb, bool three_
 }
 
 int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, double* anorm,
-              double* ainvnorm, int* status, cudaStream_t s) {
+              double* ainvnorm, int* status, cudaStream_t s, int* perm_out) {
   if (batch <= 0 || n <= 0) return 0;
   const int sms = sm_count();
   const bool fused_full = gj_is_fused_full(batch, n);
@@ -367,6 +373,7 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
     f.col_lo = 0;
     f.col_hi = ncols;
     f.full = 1;
+    f.perm_out = perm_out;
     const int grid = batch < 2 * sms ? batch : 2 * sms;
     return launch_gj_fused(f, grid, s);
   }
@@ -423,7 +430,11 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
   int* pinv = reinterpret_cast<int*>(wbuf + (size_t)batch * GJ_OUTER_NB * ncols);
   for (int off = 0; off < batch; off += 65535) {
     const int bb = min(65535, batch - off);
-    gj_perm_kernel<<<bb, 128, sizeof(int) * n, s>>>(n, piv, pinv, off);
+    if (perm_out) {
+      gj_perm_kernel<<<bb, 128, sizeof(int) * n, s>>>(n, piv, perm_out, off, 1);
+      continue;
+    }
+    gj_perm_kernel<<<bb, 128, sizeof(int) * n, s>>>(n, piv, pinv, off, 0);
     const int rows_per_cta = 32;
     const size_t usmem = sizeof(double) * (size_t)n * 4;
     if (usmem > 48 * 1024)

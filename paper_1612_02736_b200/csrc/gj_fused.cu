@@ -337,15 +337,21 @@ __global__ void __launch_bounds__(NTH, (RPT >= 8 || NTH > 256 ? 1 : 2)) gj_fused
         }
       }
       __syncthreads();
-      double* buf = S.P + (size_t)warp * n;
-      for (int r = warp; r < n; r += FU_THREADS / 32) {
-        double* rowp = Mi + (long long)r * ld;
+      if (a.perm_out) {
+        // leave the columns permuted; consumers gather their right-hand side with perm
+        int* po = a.perm_out + (long long)item * n;
+        for (int j = tid; j < n; j += FU_THREADS) po[j] = perm[j];
+      } else {
+        double* buf = S.P + (size_t)warp * n;
+        for (int r = warp; r < n; r += FU_THREADS / 32) {
+          double* rowp = Mi + (long long)r * ld;
 #pragma unroll 8
-        for (int c = lane; c < n; c += 32) buf[c] = rowp[c];
-        __syncwarp();
+          for (int c = lane; c < n; c += 32) buf[c] = rowp[c];
+          __syncwarp();
 #pragma unroll 8
-        for (int c = lane; c < n; c += 32) rowp[perm[c]] = buf[c];
-        __syncwarp();
+          for (int c = lane; c < n; c += 32) rowp[perm[c]] = buf[c];
+          __syncwarp();
+        }
       }
       __syncthreads();
       if (a.ainvnorm) {

@@ -59,10 +59,10 @@ long long hps_gj_workspace_bytes(int batch, int n, int ncols) {
 }
 
 int hps_gj_invert_batched(int batch, int n, int ncols, const hps_mat_batch* M, int* piv, void* workspace,
-                          double* anorm, double* ainvnorm, int* status, void* stream) {
+                          double* anorm, double* ainvnorm, int* status, int* perm, void* stream) {
   if (!M || !piv || !workspace || n <= 0 || ncols < n) return HPS_EINVAL;
   return gj_invert(batch, n, ncols, to_matb(M), piv, (double*)workspace, anorm, ainvnorm, status,
-                   (cudaStream_t)stream);
+                   (cudaStream_t)stream, perm);
 }
 
 long long hps_leaf_workspace_bytes(int nleaf, int p, int q) {
@@ -110,7 +110,7 @@ int hps_leaf_build(const hps_leaf_batch* L, void* stream) {
 
   // [F | S] = inv(A_ii) [I | -A_ie L]
   if ((rc = gj_invert(nl, m, m + b, dense(L->fs, sfs, m + b), piv, (double*)gjw, L->anorm, L->ainvnorm,
-                      L->status, s)))
+                      L->status, s, L->perm)))
     return rc;
 
   // H = D_fi F   (leaf.py:162; exterior rows of F are zero)
@@ -163,7 +163,7 @@ int hps_merge_build(const hps_merge_batch* Mb, void* stream) {
   if (rc) return rc;
 
   if ((rc = gj_invert(np, m3, m3 + e, dense(Mb->xs, sxs, m3 + e), piv, (double*)gjw, Mb->dnorm, Mb->xnorm,
-                      Mb->status, s)))
+                      Mb->status, s, Mb->perm)))
     return rc;
 
   // T_new = blkdiag + T_ei S   (solver.py:139-141)

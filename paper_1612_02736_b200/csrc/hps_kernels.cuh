@@ -24,8 +24,10 @@ int launch_gemm(const GemmArgs& g, int batch, int mode, cudaStream_t s);
 // workspace (see gj_workspace_doubles). On exit M_i[:, :n] = inv(A_i) (columns un-permuted),
 // M_i[:, n:] = inv(A_i) * rhs_i. anorm/ainvnorm (may be null): 1-norms before/after.
 long long gj_workspace_doubles(int batch, int n, int ncols);
+// perm_out (nullable): leave the inverse's columns permuted, M[:, j] = inv(A)[:, perm[j]], and
+// write perm (batch x n); consumers then gather right-hand sides as x[j] = b[perm[j]].
 int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, double* anorm,
-              double* ainvnorm, int* status, cudaStream_t s);
+              double* ainvnorm, int* status, cudaStream_t s, int* perm_out = nullptr);
 
 int launch_colnorm1(int batch, int n, MatB M, double* out, cudaStream_t s);
 
@@ -39,6 +41,7 @@ struct FusedArgs {
   int k_begin, k_end;  // pivot columns processed
   int col_lo, col_hi;  // columns updated (must contain [k_begin, k_end))
   int full;            // 1: norms + column un-permutation
+  int* perm_out;       // full mode: if set, columns stay permuted and perm (batch x n) is written
   int ldp, ldw, cw;    // set by the launcher
 };
 int gj_fused_panel_width(int n, int full);

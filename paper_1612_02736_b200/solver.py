@@ -111,6 +111,7 @@ class _LeafGroup:
     status: torch.Tensor = None
     consts: dict = None
     coef: torch.Tensor = None  # [6, L, P] coefficient samples (kept only in economy mode)
+    perm: torch.Tensor = None  # [L, m] column order of F / H (pivot order)
     first_row: int = 0     # global leaf row of slot 0 (G / UC regions)
 
 
@@ -129,6 +130,7 @@ class _ParentGroup:
     dnorm: torch.Tensor = None
     xnorm: torch.Tensor = None
     status: torch.Tensor = None
+    perm: torch.Tensor = None  # [npar, m3] column order of X (pivot order)
     wrap: dict = None      # singleton wrapped parent: qd, qu, pu, pd, ec, xsw, tw
 
     @property
@@ -355,11 +357,12 @@ class FactorizedSolver:
         m, b, P, c = (p - 2) ** 2, 4 * q, p * p, 4 * (p - 1)
         hslot = lay["hslot"]
         tree, plan = self.tree, self.plan
-        # leaves: h = H g   (solver.py:278)
-        for grp in self.leaf_groups:
+        # leaves: h = H g   (solver.py:278); H and F columns are in pivot order -> gather g by perm
+        leaf_perm = [grp.perm.cpu().numpy().astype(np.int64) for grp in self.leaf_groups]
+        for gi, grp in enumerate(self.leaf_groups):
             L = len(grp.ids)
             rows = grp.first_row + np.arange(L)
-            xidx = lay["G"] + rows[:, None] * m + np.arange(m)[None, :]
+            xidx = lay["G"] + rows[:, None] * m + leaf_perm[gi]
             oidx = np.stack([hslot[n] + np.arange(b) for n in grp.ids])
             up.append(gemv(L, b, m, _ext.mat(grp.h if grp.h is not None else 0, b * m, m), xidx, oidx))
             up[-1]["patch"] = ("h", self.leaf_groups.index(grp))
@@ -367,11 +370,13 @@ class FactorizedSolver:
         for grp in sorted(self.parent_groups, key=lambda g_: -g_.depth):
             m3, e = grp.m3, grp.e
             xw, x2w, ow, ah, oh = [], [], [], [], []
-            for nid in grp.ids:
+            xperm = grp.perm.cpu().numpy().astype(np.int64)
+            for slot, nid in enumerate(grp.ids):
                 ca, cb = tree.nodes[nid].children
                 en = plan.node[nid]
-                xw.append(hslot[cb] + en.pos3_b)
-                x2w.append(hslot[ca] + en.pos3_a)
+                # X's columns are in pivot order: gather the interface jump by perm
+                xw.append(hslot[cb] + en.pos3_b[xperm[slot]])
+                x2w.append(hslot[ca] + en.pos3_a[xperm[slot]])
                 ow.append(lay["W"] + en.j3)
                 ah.append(np.concatenate([hslot[ca] + en.pos1_a, hslot[cb] + en.pos2_b]))
                 oh.append((lay["hpre"][nid] if grp.wrap is not None else hslot[nid]) + np.arange(e))
@@ -413,11 +418,11 @@ class FactorizedSolver:
             down.append(gemv(len(grp.ids), m3, e, _ext.mat(grp.xs, m3 * (m3 + e), m3 + e, off=m3), xi,
                              lay["U"] + j3, aidx=lay["W"] + j3))
         # leaves: u_c[i_ci] = [F | S] [g; u_ext], fused tail stage u_c[i_ce] = L u_ext  (solver.py:325-327)
-        for grp in self.leaf_groups:
+        for gi, grp in enumerate(self.leaf_groups):
             L = len(grp.ids)
             rows = grp.first_row + np.arange(L)
             ext = np.stack([lay["U"] + plan.node[n].ext for n in grp.ids])
-            gx = lay["G"] + rows[:, None] * m + np.arange(m)[None, :]
+            gx = lay["G"] + rows[:, None] * m + leaf_perm[gi]
             base = lay["UC"] + rows[:, None] * P
             down.append(gemv(L, m, m + b, _ext.mat(grp.fs if grp.fs is not None else 0, m * (m + b), m + b),
                              np.concatenate([gx, ext], axis=1),
@@ -709,11 +714,12 @@ def _build_device(solver: FactorizedSolver, order, profile=False):
             grp.dnorm = torch.empty(npar, dtype=torch.float64, device=dev)
             grp.xnorm = torch.empty(npar, dtype=torch.float64, device=dev)
             grp.status = torch.zeros(npar, dtype=torch.int32, device=dev)
+            grp.perm = torch.empty((npar, m3), dtype=torch.int32, device=dev)
             ws = torch.empty(int(lib.hps_merge_workspace_bytes(npar, m3, e)), dtype=torch.uint8, device=dev)
             mb = _ext.MergeBatch(npar, m3, grp.n1, grp.n2, ta_ptr.data_ptr(), tb_ptr.data_ptr(), grp.lda, grp.ldb,
                                  idx.data_ptr(), 0 if same else idx.shape[1], grp.xs.data_ptr(),
                                  grp.tei.data_ptr(), grp.tnew.data_ptr(), grp.dnorm.data_ptr(),
-                                 grp.xnorm.data_ptr(), grp.status.data_ptr(), ws.data_ptr())
+                                 grp.xnorm.data_ptr(), grp.status.data_ptr(), grp.perm.data_ptr(), ws.data_ptr())
             ph.mark(f"merge-prep d{d}")
             _ext.check(lib.hps_merge_build(mb, s), "merge build")
             ph.mark(f"merge d{d} x{npar} m3={m3} e={e}")
@@ -752,12 +758,16 @@ def _leaf_build_call(grp, p, q, lib, s):
     h = torch.empty((L, b, m), dtype=torch.float64, device=dev)
     t = torch.empty((L, b, b), dtype=torch.float64, device=dev)
     ws = torch.empty(int(lib.hps_leaf_workspace_bytes(L, p, q)), dtype=torch.uint8, device=dev)
+    if grp.perm is None:
+        grp.perm = torch.empty((L, m), dtype=torch.int32, device=dev)
     cs = grp.consts
+    # F and H stay in pivot column order (no un-permutation pass); the sweeps gather g by perm
     lb = _ext.LeafBatch(L, p, q, grp.coef.data_ptr(), cs["dx"].data_ptr(), cs["dy"].data_ptr(),
                         cs["dxx"].data_ptr(), cs["dyy"].data_ptr(), cs["int_pos"].data_ptr(),
                         cs["ext_pos"].data_ptr(), cs["lift"].data_ptr(), cs["dfi"].data_ptr(),
                         cs["t0"].data_ptr(), fs.data_ptr(), h.data_ptr(), t.data_ptr(),
-                        grp.anorm.data_ptr(), grp.ainvnorm.data_ptr(), grp.status.data_ptr(), ws.data_ptr())
+                        grp.anorm.data_ptr(), grp.ainvnorm.data_ptr(), grp.status.data_ptr(),
+                        grp.perm.data_ptr(), ws.data_ptr())
     _ext.check(lib.hps_leaf_build(lb, s), "leaf build")
     return fs, h, t
 

@@ -59,7 +59,7 @@ def _gj(lib, M, n, ncols):
     ai = torch.empty(batch, dtype=torch.float64, device="cuda")
     st = torch.zeros(batch, dtype=torch.int32, device="cuda")
     rc = lib.hps_gj_invert_batched(batch, n, ncols, _ext.mat(M, n * ncols, ncols), piv.data_ptr(), ws.data_ptr(),
-                                   an.data_ptr(), ai.data_ptr(), st.data_ptr(), _stream())
+                                   an.data_ptr(), ai.data_ptr(), st.data_ptr(), None, _stream())
     assert rc == 0
     torch.cuda.synchronize()
     return piv, an, ai, st
@@ -108,3 +108,21 @@ def test_gj_flags_singular(lib):
     _, an, ai, st = _gj(lib, M, n, n)
     s = st.cpu().numpy()
     assert s[0] != 0 and s[1] == 0
+
+
+@pytest.mark.parametrize("n,batch", [(60, 3), (196, 200), (300, 2)])
+def test_gj_permuted_columns_output(lib, n, batch):
+    rng = np.random.default_rng(n + 1)
+    A = rng.standard_normal((batch, n, n)) + 2 * n ** 0.5 * np.eye(n)
+    M = torch.tensor(A.copy(), device="cuda")
+    piv = torch.empty(batch, n, dtype=torch.int32, device="cuda")
+    perm = torch.empty(batch, n, dtype=torch.int32, device="cuda")
+    ws = torch.empty(int(lib.hps_gj_workspace_bytes(batch, n, n)), dtype=torch.uint8, device="cuda")
+    rc = lib.hps_gj_invert_batched(batch, n, n, _ext.mat(M, n * n, n), piv.data_ptr(), ws.data_ptr(), None, None,
+                                   None, perm.data_ptr(), _stream())
+    assert rc == 0
+    torch.cuda.synchronize()
+    out, pm = M.cpu().numpy(), perm.cpu().numpy()
+    for i in range(batch):
+        inv = np.linalg.inv(A[i])
+        assert np.abs(out[i] - inv[:, pm[i]]).max() <= 1e-11 * np.abs(inv).max()

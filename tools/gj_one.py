@@ -22,7 +22,7 @@ for r in range(reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     lib.hps_gj_invert_batched(batch, n, ncols, _ext.mat(M, n * ncols, ncols), piv.data_ptr(), ws.data_ptr(),
-                              None, None, None, s)
+                              None, None, None, None, s)
     e1.record()
     torch.cuda.synchronize()
     times.append(e0.elapsed_time(e1))
