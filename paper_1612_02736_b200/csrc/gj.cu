@@ -332,6 +332,13 @@ struct Lookahead {
 static int factor_block(int batch, int n, int ncols, int K0, int nb, bool three_level, MatB M, int* piv,
                         int* status, MatB W, cudaStream_t s) {
   int rc;
+  static int use_cluster = -1;
+  if (use_cluster < 0) {
+    const char* e = getenv("HPS_GJ_CLUSTER");
+    use_cluster = e ? atoi(e) : 1;
+  }
+  if (three_level && use_cluster && gj_cluster_ok(n, nb))
+    return launch_gj_cluster(batch, n, K0, nb, M, piv, status, s);
   const int kin = three_level ? gj_fused_panel_width(n, 0) : nb;
   for (int k0 = K0; k0 < K0 + nb; k0 += kin) {
     const int kb = min(kin, K0 + nb - k0);

@@ -45,6 +45,9 @@ struct FusedArgs {
   int ldp, ldw, cw;    // set by the launcher
 };
 int gj_fused_panel_width(int n, int full);
+// cluster block factorisation for few large matrices (gj_cluster.cu)
+bool gj_cluster_ok(int n, int nb);
+int launch_gj_cluster(int batch, int n, int k0, int nb, MatB M, int* piv, int* status, cudaStream_t s);
 int launch_gj_fused(const FusedArgs& a, int grid, cudaStream_t s);
 
 // Leaf-stage assembly: interior rows of the collocation matrix for each leaf.
