@@ -6,19 +6,24 @@ the Chebyshev collocation nodes out. Host code mirrors the reference API; the nu
 in hand-written sm_100a CUDA kernels behind the C ABI in include/hps_b200.h.
 """
 
-from .geometry import (BoxNode, DomainTree, MeshConformityError, MergePlan, NodePlan, Rect,
-                       build_balanced_refined_tree, build_uniform_tree, count_chebyshev_dofs,
-                       enumerate_gauss_nodes, refine_near_point)
+from .geometry import (BoxNode, DomainTree, MeshConformityError, MergePlan, MeshSpec, NodePlan, Rect,
+                       build_balanced_refined_tree, build_forest, build_mesh, build_uniform_tree,
+                       count_chebyshev_dofs, enumerate_gauss_nodes, refine_near_point)
 from .model import CoefficientField, ProblemSpec, catalog, manufactured_spec
 from .solver import (FactorizedSolver, LeafSingularError, MergeSingularError, SolveState,
                      build_stage, downward_pass, solve, upward_pass)
+from .reference import ReferenceSolution, linf_error
+from .timestepping import ParabolicProblem, TimeStepConfig, be_run, cn_elliptic_spec, cn_run
+from .archive import ArchiveError, load_operators, persist_operators
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "BoxNode", "DomainTree", "MeshConformityError", "MergePlan", "NodePlan", "Rect",
-    "build_balanced_refined_tree", "build_uniform_tree", "count_chebyshev_dofs",
+    "BoxNode", "DomainTree", "MeshConformityError", "MergePlan", "MeshSpec", "NodePlan", "Rect",
+    "build_balanced_refined_tree", "build_forest", "build_mesh", "build_uniform_tree", "count_chebyshev_dofs",
     "enumerate_gauss_nodes", "refine_near_point", "CoefficientField", "ProblemSpec", "catalog",
     "manufactured_spec", "FactorizedSolver", "LeafSingularError", "MergeSingularError",
-    "SolveState", "build_stage", "downward_pass", "solve", "upward_pass",
+    "SolveState", "build_stage", "downward_pass", "solve", "upward_pass", "ReferenceSolution", "linf_error",
+    "ParabolicProblem", "TimeStepConfig", "be_run", "cn_elliptic_spec", "cn_run", "ArchiveError",
+    "load_operators", "persist_operators",
 ]

@@ -647,13 +647,7 @@ def _build_device(solver: FactorizedSolver, order, profile=False):
         L = len(ids)
         row += L
         leaf_ids.extend(ids)
-        int_pos = np.full(P, -1)
-        int_pos[sc.i_ci] = np.arange(m)
-        ext_pos = np.full(P, -1)
-        ext_pos[sc.i_ce] = np.arange(c)
-        grp.consts = {"dx": _f64(sc.dx, dev), "dy": _f64(sc.dy, dev), "dxx": _f64(sc.dxx, dev),
-                      "dyy": _f64(sc.dyy, dev), "int_pos": _i32(int_pos, dev), "ext_pos": _i32(ext_pos, dev),
-                      "lift": _f64(sc.lift, dev), "dfi": _f64(sc.dfi, dev), "t0": _f64(sc.t0, dev)}
+        grp.consts = _leaf_consts(sc, dev)
         org = torch.as_tensor(np.array([[tree.nodes[n].bounds.x1lo, tree.nodes[n].bounds.x2lo] for n in ids]),
                               dtype=torch.float64, device=dev)
         pts0 = torch.as_tensor(sc.cheb2d(), dtype=torch.float64, device=dev)
@@ -747,6 +741,18 @@ def _build_device(solver: FactorizedSolver, order, profile=False):
         else:
             grp.coef = None
     solver._layout = _layout(solver)
+
+
+def _leaf_consts(sc, dev):
+    """Device copies of a leaf shape's constants (1D operators, index maps, lift, flux parts)."""
+    P, m, c = sc.p * sc.p, sc.m, sc.c
+    int_pos = np.full(P, -1)
+    int_pos[sc.i_ci] = np.arange(m)
+    ext_pos = np.full(P, -1)
+    ext_pos[sc.i_ce] = np.arange(c)
+    return {"dx": _f64(sc.dx, dev), "dy": _f64(sc.dy, dev), "dxx": _f64(sc.dxx, dev),
+            "dyy": _f64(sc.dyy, dev), "int_pos": _i32(int_pos, dev), "ext_pos": _i32(ext_pos, dev),
+            "lift": _f64(sc.lift, dev), "dfi": _f64(sc.dfi, dev), "t0": _f64(sc.t0, dev)}
 
 
 def _leaf_build_call(grp, p, q, lib, s):

@@ -93,6 +93,12 @@ def plan_fixture():
     t = build_balanced_refined_tree(8, (0.3, 0.7), 8, tree_factory=build_uniform_tree)
     for k, v in plan_arrays(enumerate_gauss_nodes(t, 14), t).items():
         out["cfg4q14_" + k] = v
+    from specdtn.geometry import build_forest
+    lshape = ((0.0, 1.0, 0.0, 1.0), (1.0, 2.0, 0.0, 1.0), (0.0, 1.0, 1.0, 2.0))
+    t = build_forest(lshape, 2)
+    refine_near_point(t, RefinementSpec((1.0, 1.0), 1))
+    for k, v in plan_arrays(enumerate_gauss_nodes(t, 8), t).items():
+        out["lshape_" + k] = v
     save("plans.npz", **out)
 
 
@@ -222,6 +228,9 @@ if __name__ == "__main__":
     import sys as _sys
     if "--only-cn" in _sys.argv:
         cn_fixture()
+        raise SystemExit
+    if "--only-plans" in _sys.argv:
+        plan_fixture()
         raise SystemExit
     cn_fixture()
     spectral_fixture()

@@ -211,3 +211,24 @@ def test_cooperative_sweep_program_matches_graph_path():
     assert rel_maxdiff(sb.u, sa.u) <= 1e-14
     for nid in sa.leaf_solutions:
         np.testing.assert_allclose(sb.leaf_solutions[nid], sa.leaf_solutions[nid], rtol=0, atol=1e-13)
+
+
+class TestUnionDomains:
+    """Reference test_solver.py:295-311 (harmonic data reproduced on an L-shaped forest)."""
+    L = ((0.0, 1.0, 0.0, 1.0), (1.0, 2.0, 0.0, 1.0), (0.0, 1.0, 1.0, 2.0))
+
+    @pytest.mark.parametrize("refine", [False, True])
+    def test_harmonic_on_lshape(self, refine):
+        from paper_1612_02736_b200 import build_forest
+        tree = build_forest(self.L, 2)
+        if refine:
+            refine_near_point(tree, (1.0, 1.0), 1)
+        p, q = (10, 9) if not refine else (9, 8)
+        solver = build_stage(tree, catalog("laplace"), p, q)
+        f = lambda pts: pts[:, 0] ** 2 - pts[:, 1] ** 2
+        st = solver.solve(f=f)
+        for lf in tree.leaves():
+            pts = orc.leaf_points(lf.bounds, p, q)
+            assert np.abs(st.leaf_solutions[lf.id] - f(pts)).max() <= 1e-10
+        ref = orc.solve(orc.build(tree, catalog("laplace"), p, q, enumerate_gauss_nodes(tree, q)), f)
+        assert rel_maxdiff(st.u, ref["u"]) <= 1e-10

@@ -3,9 +3,9 @@ import numpy as np
 import pytest
 
 from paper_1612_02736_b200 import spectral
-from paper_1612_02736_b200.geometry import (build_balanced_refined_tree, build_uniform_tree,
-                                            enumerate_gauss_nodes, refine_near_point,
-                                            count_chebyshev_dofs)
+from paper_1612_02736_b200.geometry import (MeshSpec, build_balanced_refined_tree, build_forest, build_mesh,
+                                            build_uniform_tree, count_chebyshev_dofs, enumerate_gauss_nodes,
+                                            refine_near_point)
 from hps_testutil import golden
 
 SHAPES = ((16, 15, 0.25, 0.25), (12, 11, 1.0, 1.0), (9, 8, 0.5, 0.25),
@@ -86,3 +86,19 @@ def test_plan_config4_balanced():
 def test_chebyshev_dof_count():
     t = build_uniform_tree((0, 1, 0, 1), 4)
     assert count_chebyshev_dofs(t, 16) == (4 * 15 + 1) ** 2 == 3721
+
+
+def test_plan_refined_lshape_forest():
+    lshape = ((0.0, 1.0, 0.0, 1.0), (1.0, 2.0, 0.0, 1.0), (0.0, 1.0, 1.0, 2.0))
+    t = build_forest(lshape, 2)
+    refine_near_point(t, (1.0, 1.0), 1)
+    _check_plan("lshape_", t, enumerate_gauss_nodes(t, 8))
+
+
+def test_mesh_spec_round_trip():
+    lshape = ((0.0, 1.0, 0.0, 1.0), (1.0, 2.0, 0.0, 1.0), (0.0, 1.0, 1.0, 2.0))
+    t = build_forest(lshape, 2)
+    refine_near_point(t, (1.0, 1.0), 1)
+    t2 = build_mesh(MeshSpec.from_json(t.mesh_spec.to_json()))
+    assert [n.bounds for n in t.nodes] == [n.bounds for n in t2.nodes]
+    assert [n.children for n in t.nodes] == [n.children for n in t2.nodes]
