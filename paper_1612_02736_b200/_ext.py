@@ -78,8 +78,8 @@ def load(build_if_missing: bool = True):
     with _lock:
         if _lib is not None:
             return _lib
-        path = build_ext.LIB
-        if not os.path.exists(path) or not build_ext.up_to_date():
+        path = os.environ.get("HPS_B200_LIB") or build_ext.LIB  # override: A/B tuning builds only
+        if path == build_ext.LIB and (not os.path.exists(path) or not build_ext.up_to_date()):
             if not build_if_missing:
                 raise ExtensionError(f"HPS CUDA extension missing: {path}")
             build_ext.build()

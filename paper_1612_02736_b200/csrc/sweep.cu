@@ -21,6 +21,64 @@ namespace hps {
 
 constexpr int SW_THREADS = 256;
 
+// every sweep launch carries the programmatic-serialization attribute (HPS_PDL=0 disables)
+static bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("HPS_PDL");
+    on = (e && atoi(e) == 0) ? 0 : 1;
+  }
+  return on != 0;
+}
+
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
+// x gather into shared memory: dst[k*ld + j] = pool[xi[k]][j] (- pool[x2[k]][j]) for k < kc,
+// j < nrhs; zero for kc <= k < kp or j >= nrhs. GU elements per thread are issued together so
+// the index -> value load chains overlap: one memory round trip per GU elements, not per element
+// (the per-element loop left the multi-RHS leaf steps stalled on the gather, r01 ncu).
+template <int NRP, int GU = 8>
+__device__ __forceinline__ void gather_x(double* dst, int ld, const int* __restrict__ xi,
+                                         const int* __restrict__ x2, const double* pool, int nrhs, int kc,
+                                         int kp) {
+  const int tot = kp * NRP, nth = blockDim.x;
+  for (int e0 = threadIdx.x; e0 < tot; e0 += GU * nth) {
+    int i1[GU], i2[GU];
+#pragma unroll
+    for (int u = 0; u < GU; ++u) {
+      const int e = e0 + u * nth, k = e / NRP;
+      const bool ok = e < tot && k < kc && e - k * NRP < nrhs;
+      i1[u] = ok ? __ldg(xi + k) : -1;
+      i2[u] = (ok && x2) ? __ldg(x2 + k) : -1;
+    }
+    double v[GU];
+#pragma unroll
+    for (int u = 0; u < GU; ++u) {
+      const int e = e0 + u * nth, k = e / NRP, j = e - k * NRP;
+      v[u] = i1[u] >= 0 ? pool[(long long)i1[u] * nrhs + j] : 0.0;
+      if (i2[u] >= 0) v[u] -= pool[(long long)i2[u] * nrhs + j];
+    }
+#pragma unroll
+    for (int u = 0; u < GU; ++u) {
+      const int e = e0 + u * nth, k = e / NRP, j = e - k * NRP;
+      if (e < tot) dst[k * ld + j] = v[u];
+    }
+  }
+}
+
 template <int NR>
 __global__ void __launch_bounds__(SW_THREADS) gemv_gather_kernel(GemvArgs a, int rows_per_cta, int kchunk,
                                                                  int batch_off) {
@@ -39,6 +97,7 @@ __global__ void __launch_bounds__(SW_THREADS) gemv_gather_kernel(GemvArgs a, int
   const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
   double* pool = a.pool;
 
+  pdl_trigger();
   for (int e = tid; e < (r1 - r0) * NR; e += SW_THREADS) part[e] = 0.0;
   for (int r = r0 + tid; r < r1; r += SW_THREADS) {
     // start streaming this CTA's operator rows into L2 while x is gathered
@@ -47,6 +106,7 @@ __global__ void __launch_bounds__(SW_THREADS) gemv_gather_kernel(GemvArgs a, int
     const uintptr_t hi = (reinterpret_cast<uintptr_t>(rp + K) + 15) & ~(uintptr_t)15;
     prefetch_l2_bulk(reinterpret_cast<const void*>(lo), (unsigned)(hi - lo));
   }
+  pdl_wait();
 
   for (int k0 = 0; k0 < K; k0 += kchunk) {
     const int kc = min(kchunk, K - k0);
@@ -99,7 +159,7 @@ __global__ void __launch_bounds__(SW_THREADS) gemv_gather_kernel(GemvArgs a, int
 // lane group reads one 32-byte sector per row, 8 loads in flight per lane), X is gathered into
 // shared memory chunk by chunk with a padded stride (conflict-free B fragments).
 template <int NRP, bool VEC>
-__global__ void __launch_bounds__(256) gemv_dmma_kernel(GemvArgs a, int rpc, int kchunk, int batch_off) {
+__global__ void __launch_bounds__(256, 4) gemv_dmma_kernel(GemvArgs a, int rpc, int kchunk, int batch_off) {
   extern __shared__ double xs[];
   // VEC: each lane loads A[r][k+2t .. k+2t+1] as one 16-byte load and uses the two halves as
   // the A fragments of two "virtual" k4 steps; B fragments follow the same k permutation.
@@ -129,20 +189,14 @@ __global__ void __launch_bounds__(256) gemv_dmma_kernel(GemvArgs a, int rpc, int
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int n = 0; n < NT; ++n) acc[i][n][0] = acc[i][n][1] = 0.0;
+  pdl_trigger();
+  pdl_wait();
 
   for (int k0 = 0; k0 < K; k0 += kchunk) {
     const int kc = min(kchunk, K - k0);
     const int kcp = VEC ? (kc + 7) & ~7 : (kc + 3) & ~3;
     __syncthreads();
-    for (int e = tid; e < kcp * NRP; e += blockDim.x) {
-      const int k = e / NRP, j = e - k * NRP;
-      double v = 0.0;
-      if (j < nrhs && k < kc) {
-        v = pool[(long long)xi[k0 + k] * nrhs + j];
-        if (x2) v -= pool[(long long)x2[k0 + k] * nrhs + j];
-      }
-      xs[k * XLD + j] = v;
-    }
+    gather_x<NRP, 4>(xs, XLD, xi + k0, x2 ? x2 + k0 : nullptr, pool, nrhs, kc, kcp);
     __syncthreads();
     if (VEC) {
       const int step = WK * 8;
@@ -365,7 +419,7 @@ __device__ __forceinline__ void rows_dot(const double* __restrict__ A, long long
 __host__ __device__ inline int lanes_for(int K) { return K <= 16 ? 4 : (K <= 48 ? 8 : (K <= 128 ? 16 : 32)); }
 
 // One work unit of a sweep step: item `item`, row chunk `chunk` of `nchunks` (rows_per_cta rows).
-template <int NR, bool VEC, int RB = 2, int U = 4>
+template <int NR, bool VEC, int RB = 2, int U = 4, bool PDL = false>
 __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chunk, int nchunks, int rows_per_cta,
                                            double* sm) {
   double* xs = sm;                        // K x NR
@@ -384,15 +438,8 @@ __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chun
     const uintptr_t hi = (reinterpret_cast<uintptr_t>(rp + K) + 15) & ~(uintptr_t)15;
     prefetch_l2_bulk(reinterpret_cast<const void*>(lo), (unsigned)(hi - lo));
   }
-  for (int e = threadIdx.x; e < K * NR; e += blockDim.x) {
-    const int k = e / NR, j = e - k * NR;
-    double v = 0.0;
-    if (j < nrhs) {
-      v = pool[(long long)xi[k] * nrhs + j];
-      if (x2) v -= pool[(long long)x2[k] * nrhs + j];
-    }
-    xs[e] = v;
-  }
+  if (PDL) pdl_wait();
+  gather_x<NR>(xs, NR, xi, x2, pool, nrhs, K, K);
   __syncthreads();
   rows_dot<NR, VEC, RB, U>(Ai, a.A.ld, a.R, r0, r1, K, lanes_for(K), xs,
                            a.aidx ? a.aidx + (long long)item * a.ostride : nullptr,
@@ -415,7 +462,8 @@ __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chun
 template <int NR, bool VEC, int RB = 2, int U = 4>
 __global__ void __launch_bounds__(256) sweep_kernel(GemvArgs a, int rows_per_cta, int batch_off) {
   extern __shared__ double sm[];
-  sweep_unit<NR, VEC, RB, U>(a, blockIdx.y + batch_off, blockIdx.x, gridDim.x, rows_per_cta, sm);
+  pdl_trigger();
+  sweep_unit<NR, VEC, RB, U, true>(a, blockIdx.y + batch_off, blockIdx.x, gridDim.x, rows_per_cta, sm);
 }
 
 // Whole solve program in one cooperative launch: the steps run in order, separated by a
@@ -452,7 +500,7 @@ static void launch_nr(const GemvArgs& a, cudaStream_t s) {
   const int gx = (a.R + rows - 1) / rows;
   for (int off = 0; off < a.nitems; off += 65535) {
     dim3 grid(gx, min(65535, a.nitems - off));
-    gemv_gather_kernel<NR><<<grid, SW_THREADS, smem, s>>>(a, rows, kchunk, off);
+    launch_k(gemv_gather_kernel<NR>, grid, dim3(SW_THREADS), smem, s, a, rows, kchunk, off);
   }
 }
 
@@ -477,9 +525,9 @@ static void launch_dmma(const GemvArgs& a, cudaStream_t s) {
   for (int off = 0; off < a.nitems; off += 65535) {
     dim3 grid(gx, min(65535, a.nitems - off));
     if (vec)
-      gemv_dmma_kernel<NRP, true><<<grid, 256, smem, s>>>(a, rpc, kchunk, off);
+      launch_k(gemv_dmma_kernel<NRP, true>, grid, dim3(256), smem, s, a, rpc, kchunk, off);
     else
-      gemv_dmma_kernel<NRP, false><<<grid, 256, smem, s>>>(a, rpc, kchunk, off);
+      launch_k(gemv_dmma_kernel<NRP, false>, grid, dim3(256), smem, s, a, rpc, kchunk, off);
   }
 }
 
@@ -548,18 +596,45 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
   for (int off = 0; off < a.nitems; off += 65535) {
     dim3 grid(gx, min(65535, a.nitems - off));
     switch (variant) {
-      case 1: sweep_kernel<NR, false, 1, 8><<<grid, 256, smem, s>>>(a, rows, off); break;
-      case 2: sweep_kernel<NR, true, 1, 4><<<grid, 256, smem, s>>>(a, rows, off); break;
-      case 3: sweep_kernel<NR, false, 1, 4><<<grid, 256, smem, s>>>(a, rows, off); break;
-      case 4: sweep_kernel<NR, true, 2, 2><<<grid, 256, smem, s>>>(a, rows, off); break;
-      default: sweep_kernel<NR, false, 2, 4><<<grid, 256, smem, s>>>(a, rows, off); break;
+      case 1: launch_k(sweep_kernel<NR, false, 1, 8>, grid, dim3(256), smem, s, a, rows, off); break;
+      case 2: launch_k(sweep_kernel<NR, true, 1, 4>, grid, dim3(256), smem, s, a, rows, off); break;
+      case 3: launch_k(sweep_kernel<NR, false, 1, 4>, grid, dim3(256), smem, s, a, rows, off); break;
+      case 4: launch_k(sweep_kernel<NR, true, 2, 2>, grid, dim3(256), smem, s, a, rows, off); break;
+      default: launch_k(sweep_kernel<NR, false, 2, 4>, grid, dim3(256), smem, s, a, rows, off); break;
     }
   }
   return true;
 }
 
+// One-row steps (split-K reductions with A = ones, the Dirichlet copy): one thread per
+// (item, rhs), so thousands of tiny items do not each occupy a CTA.
+__global__ void __launch_bounds__(256) gemv_row1_kernel(GemvArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)a.nitems * a.nrhs) return;
+  const int item = (int)(e / a.nrhs), j = (int)(e - (long long)item * a.nrhs);
+  const double* A = a.A.get(item);
+  const int* xi = a.xidx + (long long)item * a.xstride;
+  const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
+  double acc = 0.0;
+  for (int k = 0; k < a.K; ++k) {
+    double v = a.pool[(long long)xi[k] * a.nrhs + j];
+    if (x2) v -= a.pool[(long long)x2[k] * a.nrhs + j];
+    acc = fma(A[k], v, acc);
+  }
+  const long long o = (long long)a.oidx[(long long)item * a.ostride] * a.nrhs + j;
+  if (a.aidx) acc += a.pool[(long long)a.aidx[(long long)item * a.ostride] * a.nrhs + j];
+  a.pool[o] = acc;
+}
+
 int launch_gemv_gather(const GemvArgs& a, cudaStream_t s) {
   if (a.nitems <= 0 || a.R <= 0) return 0;
+  if (a.R == 1 && !a.mode2 && a.K <= 64) {
+    const long long n = (long long)a.nitems * a.nrhs;
+    launch_k(gemv_row1_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, a);
+    return cudaGetLastError() == cudaSuccess ? 0 : 2;
+  }
   if (a.nrhs <= 2) {
     const bool ok = a.nrhs == 1 ? launch_sweep<1>(a, s) : launch_sweep<2>(a, s);
     if (ok) return cudaGetLastError() == cudaSuccess ? 0 : 2;
