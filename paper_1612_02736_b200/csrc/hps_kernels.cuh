@@ -99,6 +99,8 @@ struct GemvArgs {
   long long ostride;
 };
 int launch_gemv_gather(const GemvArgs& a, cudaStream_t s);
+// TMA-fed multi-RHS path for large leaf levels (sweep_tma.cu); false = not applicable
+bool launch_gemv_tma(const GemvArgs& a, cudaStream_t s);
 
 // Whole sweep program in one cooperative launch (nrhs <= 2): steps separated by grid barriers.
 struct SweepStep {

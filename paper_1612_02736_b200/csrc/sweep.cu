@@ -639,6 +639,7 @@ int launch_gemv_gather(const GemvArgs& a, cudaStream_t s) {
     const bool ok = a.nrhs == 1 ? launch_sweep<1>(a, s) : launch_sweep<2>(a, s);
     if (ok) return cudaGetLastError() == cudaSuccess ? 0 : 2;
   }
+  if (a.nrhs > 2 && launch_gemv_tma(a, s)) return cudaGetLastError() == cudaSuccess ? 0 : 2;
   if (a.mode2) {
     // second stage for the chunked / multi-RHS paths: separate launch after the first
     GemvArgs b = a;

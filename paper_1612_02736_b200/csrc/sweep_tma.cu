@@ -1,0 +1,437 @@
+// Multi-RHS leaf sweep steps (3..16 right-hand sides) fed by TMA: Y (R x nrhs) = A (R x K) X.
+//
+// The leaf operators of one shape group are one contiguous [nitems*R][K] row-major array, so a
+// single 2D tensor map covers the whole level. A persistent CTA (one per SM) walks its items;
+// a producer warp streams 16-column slabs of an item's R rows (R <= 256) into a ring of
+// shared-memory stages with cp.async.bulk.tensor (128-byte swizzle, mbarrier complete_tx), so
+// up to NS x R x 128 bytes per SM are in flight regardless of the consumers' progress. The 8
+// consumer warps own fixed 8-row m-tiles (tile w, w+8, w+16, w+24) and run DMMA m8n8k4 on
+// conflict-free swizzled A fragments against the item's gathered X (K x NRP, padded stride).
+// X of the next item is gathered with cp.async while the current item computes (double
+// buffer). mode2 = 1 (leaf down) also applies the tail y2 = A2 x[K-K2:K) (the shared lift L).
+//
+// Why: at 16 RHS the leaf steps are 4 flop/byte, so the kernel has to keep HBM and the DMMA
+// pipes busy at once; the register-streaming gemv_dmma_kernel (sweep.cu) ran the config-5 leaf
+// downward step at 3.2 TB/s with its loads exposed (long-scoreboard stalls); this kernel runs it
+// at 4.1 TB/s (1.62 vs 2.05 ms, 16 RHS). Measured pitfalls: a guarded DMMA compiles to a
+// predicated one that still occupies the tensor pipe (hence the per-tile-count dispatch), and
+// with only 8 consumer warps per SM the short leaf upward operators (R = 4q) stay faster on
+// the 32-warp register kernel, so only R >= 128 comes here.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
+#include "hps_common.cuh"
+#include "hps_kernels.cuh"
+
+namespace hps {
+
+namespace {
+
+constexpr int TM_CONSUMERS = 8;
+constexpr int TM_THREADS = 32 * (TM_CONSUMERS + 1);
+constexpr int TM_MAXT = 4;  // m-tiles per consumer warp (R <= 256)
+
+__device__ __forceinline__ uint32_t tma_smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(tma_smem_addr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(tma_smem_addr(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tma_smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n"
+      "}\n" ::"r"(tma_smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          tma_smem_addr(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(tma_smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(tma_smem_addr(dst)), "l"(src) : "memory");
+}
+// DMMA without the volatile qualifier: no side effects, so the compiler may interleave the
+// fragment loads of the next k-step with the current tensor ops
+__device__ __forceinline__ void dmma_nv(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(TM_CONSUMERS * 32) : "memory"); }
+
+
+}  // namespace
+
+// One pipeline stage of MMAs for a warp owning T m-tiles (tile = warp + 8 i): SPS slabs of 16
+// columns, 4 k4-steps each; even / odd k4 steps accumulate into separate sets.
+template <int T, int NT, int XLD, int SPS>
+__device__ __forceinline__ void stage_mma(double (&acc)[2][TM_MAXT][NT][2], const unsigned char* base, int slot,
+                                          int sb_bytes, int nq, const double* xc, int k0, const int (&aoff)[4],
+                                          int warp, int g, int t) {
+#pragma unroll
+  for (int q = 0; q < SPS; ++q) {
+    if (q >= nq) break;
+    const double* slab = reinterpret_cast<const double*>(base + (size_t)(slot * SPS + q) * sb_bytes);
+#pragma unroll
+    for (int k4 = 0; k4 < 4; ++k4) {
+      const int kk = k0 + q * 16 + k4 * 4 + t;
+      double bv[NT];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) bv[n] = xc[kk * XLD + n * 8 + g];
+      double av[T];
+#pragma unroll
+      for (int i = 0; i < T; ++i) av[i] = slab[(warp + i * TM_CONSUMERS) * 128 + aoff[k4]];
+#pragma unroll
+      for (int i = 0; i < T; ++i)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) dmma_nv(acc[k4 & 1][i][n][0], acc[k4 & 1][i][n][1], av[i], bv[n]);
+    }
+  }
+}
+
+constexpr int TM_GMAX = 12;  // x-gather copy units per consumer thread
+
+template <int NRP, int SPS>
+__global__ void __launch_bounds__(TM_THREADS, 1)
+    gemv_tma_kernel(const __grid_constant__ CUtensorMap tm, GemvArgs a, int ns, int kst, int sb_bytes) {
+  constexpr int sps = SPS;
+  extern __shared__ unsigned char smraw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  constexpr int XLD = NRP + 4;
+  constexpr int NT = NRP / 8;
+  const int R = a.R, K = a.K, nrhs = a.nrhs;
+  // kst: stages per item, each sps 16-column slabs of sb_bytes (one TMA box each)
+  const int kp = kst * sps * 16;
+  const int nslab = (K + 15) >> 4;
+  double* xbuf = reinterpret_cast<double*>(base + (size_t)ns * sps * sb_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + 2 * (size_t)kp * XLD);
+  uint64_t* empty = full + ns;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const unsigned slab_tx = (unsigned)R * 128u;
+
+  if (tid == 0) {
+    for (int s = 0; s < ns; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, TM_CONSUMERS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  pdl_trigger();
+
+  if (warp == TM_CONSUMERS) {
+    // ---- producer: operator slabs never depend on the previous kernel, start right away
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm) : "memory");
+      int slot = 0;
+      unsigned ph = 0;
+      bool first = true;
+      for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) {
+        for (int ks = 0; ks < kst; ++ks) {
+          if (!first) mbar_wait(empty + slot, ph ^ 1u);
+          const int nq = min(sps, nslab - ks * sps);  // no fully out-of-range boxes
+          mbar_expect_tx(full + slot, slab_tx * nq);
+          for (int q = 0; q < nq; ++q)
+            tma_load_2d(base + (size_t)(slot * sps + q) * sb_bytes, &tm, (ks * sps + q) * 16, item * R, full + slot);
+          if (++slot == ns) {
+            slot = 0;
+            ph ^= 1u;
+            first = false;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumers
+  // x-gather plan (same for every item): unit u of this thread = (row, first rhs, width)
+  const bool wide = (nrhs % 2 == 0);
+  const int upr = wide ? nrhs / 2 : nrhs;  // copy units per row
+  const int nunits = K * upr;
+  int urow[TM_GMAX], ucol[TM_GMAX];
+#pragma unroll
+  for (int u = 0; u < TM_GMAX; ++u) {
+    const int e = tid + u * TM_CONSUMERS * 32;
+    urow[u] = e < nunits ? e / upr : -1;
+    ucol[u] = e < nunits ? (e - (e / upr) * upr) * (wide ? 2 : 1) : 0;
+  }
+  int nidx[TM_GMAX];
+  auto load_idx = [&](int item) {
+    const int* xi = a.xidx + (long long)item * a.xstride;
+#pragma unroll
+    for (int u = 0; u < TM_GMAX; ++u) nidx[u] = urow[u] >= 0 ? __ldg(xi + urow[u]) : 0;
+  };
+  auto issue_copies = [&](double* xb) {
+#pragma unroll
+    for (int u = 0; u < TM_GMAX; ++u) {
+      if (urow[u] < 0) continue;
+      const double* src = a.pool + (long long)nidx[u] * nrhs + ucol[u];
+      double* dst = xb + urow[u] * XLD + ucol[u];
+      if (wide)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(tma_smem_addr(dst)), "l"(src) : "memory");
+      else
+        cp_async8(dst, src);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+
+  for (int e = tid; e < 2 * kp * XLD; e += TM_CONSUMERS * 32) xbuf[e] = 0.0;
+  consumers_sync();
+  pdl_wait();  // the pool (x) is produced by the previous step
+  if (blockIdx.x < a.nitems) {
+    load_idx(blockIdx.x);
+    issue_copies(xbuf);
+  }
+  // indices of the item after next are loaded one item ahead of their copies, so neither the
+  // index loads nor the copies sit on the consumers' critical path
+  if (blockIdx.x + gridDim.x < a.nitems) load_idx(blockIdx.x + gridDim.x);
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  consumers_sync();
+
+  // A fragment rows: lanes g = 0..3 take even rows, 4..7 odd rows of an 8-row tile, so both
+  // half-warps read 8 distinct 16-byte chunks of the 128B-swizzled slab (no bank conflicts)
+  const int rg = ((g & 3) << 1) | (g >> 2);
+  int aoff[4];
+#pragma unroll
+  for (int k4 = 0; k4 < 4; ++k4) {
+    const int c = k4 * 4 + t;
+    aoff[k4] = rg * 16 + ((((c >> 1) ^ rg) << 1) | (c & 1));
+  }
+  const int mt = (R + 7) >> 3;
+  const int ntw = warp < mt ? (mt - warp + TM_CONSUMERS - 1) / TM_CONSUMERS : 0;  // m-tiles of this warp
+  int slot = 0;
+  unsigned ph = 0;
+  int it = 0;
+  for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, ++it) {
+    const double* xc = xbuf + (size_t)(it & 1) * kp * XLD;
+    double* xn = xbuf + (size_t)((it + 1) & 1) * kp * XLD;
+    // two accumulator sets (even / odd k4 steps): twice the independent DMMA chains per warp
+    double acc[2][TM_MAXT][NT][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int i = 0; i < TM_MAXT; ++i)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) acc[h][i][n][0] = acc[h][i][n][1] = 0.0;
+    const int nxt = item + gridDim.x;
+    if (nxt < a.nitems) issue_copies(xn);  // indices loaded during the previous item
+    if (nxt + (int)gridDim.x < a.nitems) load_idx(nxt + gridDim.x);
+    // output rows of this item, loaded ahead of the epilogue
+    const int* oi = a.oidx + (long long)item * a.ostride;
+    const int* ai = a.aidx ? a.aidx + (long long)item * a.ostride : nullptr;
+    int orows[TM_MAXT], arows[TM_MAXT];
+#pragma unroll
+    for (int i = 0; i < TM_MAXT; ++i) {
+      const int r = (warp + i * TM_CONSUMERS) * 8 + rg;
+      orows[i] = r < R ? __ldg(oi + r) : 0;
+      arows[i] = (ai && r < R) ? __ldg(ai + r) : -1;
+    }
+    for (int ks = 0; ks < kst; ++ks) {
+      mbar_wait(full + slot, ph);
+      const int nq = min(sps, nslab - ks * sps);
+      // the tile count is warp-uniform: dispatch to a branch-free body per count (a guarded
+      // DMMA compiles to a predicated one, which still occupies the tensor pipe)
+      switch (ntw) {
+        case 1: stage_mma<1, NT, XLD, SPS>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
+        case 2: stage_mma<2, NT, XLD, SPS>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
+        case 3: stage_mma<3, NT, XLD, SPS>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
+        case 4: stage_mma<4, NT, XLD, SPS>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
+        default: break;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + slot);
+      if (++slot == ns) {
+        slot = 0;
+        ph ^= 1u;
+      }
+    }
+    // epilogue: y rows -> pool (+ add rows)
+#pragma unroll
+    for (int i = 0; i < TM_MAXT; ++i) {
+      const int r = (warp + i * TM_CONSUMERS) * 8 + rg;
+      if (r >= R) continue;
+      const long long orow = (long long)orows[i] * nrhs;
+      const long long arow = arows[i] >= 0 ? (long long)arows[i] * nrhs : -1;
+#pragma unroll
+      for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = n * 8 + 2 * t + h;
+          if (j < nrhs) {
+            double v = acc[0][i][n][h] + acc[1][i][n][h];
+            if (arow >= 0) v += a.pool[arow + j];
+            a.pool[orow + j] = v;
+          }
+        }
+    }
+    if (a.mode2 == 1) {
+      // tail: y2 = A2 x[K-K2:K); A2 shared by the level (lift L), read through L1
+      const double* A2 = a.A2.get(item);
+      const int ld2 = a.A2.ld, K2 = a.K2, R2 = a.R2, x0 = K - K2;
+      const int* o2 = a.o2idx + (long long)item * R2;
+      const int* a2 = a.a2idx ? a.a2idx + (long long)item * R2 : nullptr;
+      for (int tile = warp; tile * 8 < R2; tile += TM_CONSUMERS) {
+        const int ra = tile * 8 + g;
+        const double* arow2 = A2 + (long long)(ra < R2 ? ra : 0) * ld2;
+        double c2[NT][2];
+#pragma unroll
+        for (int n = 0; n < NT; ++n) c2[n][0] = c2[n][1] = 0.0;
+        int k = 0;
+        for (; k + 16 <= K2; k += 16) {
+          double av[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) av[q] = ra < R2 ? __ldg(arow2 + k + 4 * q + t) : 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+              dmma8x8x4(c2[n][0], c2[n][1], av[q], xc[(x0 + k + 4 * q + t) * XLD + n * 8 + g]);
+        }
+        for (; k < K2; k += 4) {
+          const int kk = k + t;
+          const double av = (ra < R2 && kk < K2) ? __ldg(arow2 + kk) : 0.0;
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            const double bv = (kk < K2) ? xc[(x0 + kk) * XLD + n * 8 + g] : 0.0;
+            dmma8x8x4(c2[n][0], c2[n][1], av, bv);
+          }
+        }
+        if (ra < R2) {
+          const long long orow = (long long)o2[ra] * nrhs;
+          const long long arow = a2 ? (long long)a2[ra] * nrhs : -1;
+#pragma unroll
+          for (int n = 0; n < NT; ++n)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int j = n * 8 + 2 * t + h;
+              if (j < nrhs) {
+                double v = c2[n][h];
+                if (arow >= 0) v += a.pool[arow + j];
+                a.pool[orow + j] = v;
+              }
+            }
+        }
+      }
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    consumers_sync();  // next X landed for everyone; this X no longer read
+  }
+}
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool tma_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("HPS_SWEEP_TMA");
+    on = (e && atoi(e) == 0) ? 0 : 1;
+  }
+  return on != 0;
+}
+
+}  // namespace
+
+// Returns true when the step was launched here; false leaves it to the generic kernels.
+bool launch_gemv_tma(const GemvArgs& a, cudaStream_t s) {
+  if (!tma_enabled()) return false;
+  if (a.nrhs <= 2 || a.nrhs > 16 || a.x2idx || a.A.ptrs || a.mode2 == 2) return false;
+  // the leaf downward step (R = (p-2)^2 >= 128 rows); shorter operators (leaf upward, R = 4q)
+  // measured faster on the register-streaming kernel, whose 32 warps/SM hide more latency
+  if (a.R < 128 || a.R > 256 || a.K < 16 || a.nitems < 148) return false;
+  if (a.A.stride != (long long)a.R * a.A.ld || (a.A.ld * 8) % 16 != 0) return false;
+  const double* gbase = a.A.base + a.A.off;
+  if (reinterpret_cast<uintptr_t>(gbase) % 16 != 0) return false;
+  if (a.mode2 == 1 && (a.K2 > a.K || a.R2 <= 0)) return false;
+  const int upr = a.nrhs % 2 == 0 ? a.nrhs / 2 : a.nrhs;
+  if ((long long)a.K * upr > 12LL * 256) return false;  // TM_GMAX units per consumer thread
+  if (a.nrhs % 2 == 0 && reinterpret_cast<uintptr_t>(a.pool) % 16 != 0) return false;
+  auto enc = encode_fn();
+  if (!enc) return false;
+
+  const int nrp = a.nrhs <= 8 ? 8 : 16;
+  const int xld = nrp + 4;
+  const int nslab = (a.K + 15) / 16;
+  const int sb = ((a.R * 128 + 1023) / 1024) * 1024;
+  const size_t budget = 220 * 1024;
+  // one 16-column slab per stage (wider stages measured no faster on config 5)
+  int sps = 1;
+  int ns = 0, kst = 0;
+  size_t smem = 0;
+  for (; sps >= 1; sps >>= 1) {
+    kst = (nslab + sps - 1) / sps;
+    const size_t xbytes = 2 * sizeof(double) * (size_t)kst * sps * 16 * xld;
+    ns = 8;
+    while (ns > 2 && 1024 + (size_t)ns * sps * sb + xbytes + 16 * ns > budget) --ns;
+    smem = 1024 + (size_t)ns * sps * sb + xbytes + 16 * (size_t)ns;
+    if (smem <= budget && (ns >= 3 || sps == 1)) break;
+  }
+  if (sps < 1 || smem > budget) return false;
+
+  CUtensorMap tm;
+  const cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)a.nitems * a.R};
+  const cuuint64_t strides[1] = {(cuuint64_t)a.A.ld * 8};
+  const cuuint32_t box[2] = {16, (cuuint32_t)a.R};
+  const cuuint32_t estr[2] = {1, 1};
+  if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(gbase), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = a.nitems < sms ? a.nitems : sms;
+  using KFn = void (*)(const CUtensorMap, GemvArgs, int, int, int);
+  const KFn k = nrp == 16 ? gemv_tma_kernel<16, 1> : gemv_tma_kernel<8, 1>;
+  static bool configured[2] = {};
+  if (!configured[nrp == 16]) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
+    configured[nrp == 16] = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(TM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, tm, a, ns, kst, sb) == cudaSuccess;
+}
+
+}  // namespace hps

@@ -125,7 +125,8 @@ def test_resonant_leaf_raises():
         build_stage(tree, catalog("helmholtz", kappa=np.sqrt(2.0) * np.pi), 20, 19)
 
 
-@pytest.mark.parametrize("nrhs,n,p", [(1, 4, 10), (2, 4, 10), (3, 4, 10), (8, 4, 10), (16, 4, 10), (16, 16, 12)])
+@pytest.mark.parametrize("nrhs,n,p", [(1, 4, 10), (2, 4, 10), (3, 4, 10), (8, 4, 10), (16, 4, 10), (16, 16, 12),
+                                       (5, 16, 16), (16, 16, 16), (11, 32, 10)])
 def test_multi_rhs_device_solve_matches_single(nrhs, n, p):
     import torch
     tree = build_uniform_tree(UNIT, n)
