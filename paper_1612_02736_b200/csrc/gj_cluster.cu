@@ -1,14 +1,20 @@
 // Block factorisation for FEW LARGE matrices (top-of-tree merges): one thread-block cluster of
 // CL CTAs per matrix holds the n x nb column block in distributed shared memory (CTA c owns rows
 // [c*rl, (c+1)*rl)), and runs Gauss-Jordan with partial pivoting column by column:
-//   1. every CTA finds its best candidate row (|value|, ties -> smallest row) and publishes it,
-//   2. cluster barrier; every CTA reads the CL candidates through DSMEM and picks the winner
-//      (LAPACK rule), then copies the pivot row and the displaced row cj into local buffers,
-//   3. cluster barrier; every CTA eliminates its own rows over the nb block columns, the owners
-//      of rows cj / pr write the scaled pivot row / the displaced row.
-// Two cluster barriers per column and no global traffic inside the block; the whole GPU works
-// on the trailing update afterwards (gj.cu). Replaces, for batch x ceil(n/256) < 64, the
-// one-SM-per-matrix inner level whose latency dominated the root merges.
+//   1. every CTA finds its best candidate row (|value|, ties -> smallest row) and publishes it
+//      together with the row currently at the pivot position,
+//   2. one cluster barrier; every CTA reads the CL candidates through DSMEM and picks the winner
+//      (LAPACK rule), then swaps / eliminates its own rows.
+// The elimination is blocked (SB = 8 columns): inside a sub-block only its 8 columns are
+// eliminated (row interchanges are applied to all nb columns at once), and at the end of the
+// sub-block the other nb - 8 columns get the accumulated transform as one DMMA product
+//     C <- D C + W C_piv     (W: the sub-block's n x 8 GJ multipliers, C_piv: its 8 pivot
+//                             rows before the transform, D: identity with pivot rows zeroed)
+// — the same identity the outer blocked scheme (gj.cu) uses with K = nb. Per column that leaves
+// a 8-wide rank-1 update instead of a 64-wide one (the r01 profile had the 64-wide scalar
+// elimination at ~40 % of the kernel's stall samples, 373 us per 1920 x 64 block).
+// The whole GPU works on the trailing update afterwards (gj.cu). Replaces, for batch x
+// ceil(n/256) < 64, the one-SM-per-matrix inner level whose latency dominated the root merges.
 #include <cooperative_groups.h>
 
 #include "hps_common.cuh"
@@ -18,9 +24,22 @@ namespace cg = cooperative_groups;
 
 namespace hps {
 
+#ifdef GC_PROFILE
+__device__ long long gc_prof[8];
+#define GC_T(i)                                                  \
+  if (threadIdx.x == 0 && blockIdx.x == 0) {                     \
+    const long long now = clock64();                             \
+    gc_prof[i] += now - gc_last;                                 \
+    gc_last = now;                                               \
+  }
+#else
+#define GC_T(i)
+#endif
+
 constexpr int GC_CL = 8;         // CTAs per cluster (portable size)
 constexpr int GC_THREADS = 256;
 constexpr int GC_NBMAX = 64;
+constexpr int GC_SB = 8;         // sub-block width
 
 struct GcArgs {
   int batch, n, k0, nb;
@@ -30,27 +49,43 @@ struct GcArgs {
   int rl;  // rows per CTA
 };
 
+// shared-memory layout (doubles) shared by the kernel and gj_cluster_smem
+struct GcLayout {
+  int rl, nb, ldb;
+  __host__ __device__ GcLayout(int rl_, int nb_) : rl(rl_), nb(nb_), ldb(nb_ + 1) {}
+  static constexpr int BOX = 2 + GC_NBMAX;                           // best, row id, candidate row
+  __host__ __device__ size_t b() const { return 0; }                   // rl x ldb own rows
+  __host__ __device__ size_t box() const { return (size_t)rl * ldb; }  // [2][CL][BOX] inbox
+  __host__ __device__ size_t cjrow() const { return box() + 2 * GC_CL * BOX; }  // [2][NBMAX]
+  __host__ __device__ size_t cp() const { return cjrow() + 2 * GC_NBMAX; }      // [SB][NBMAX+1]
+  __host__ __device__ size_t red() const { return cp() + GC_SB * (GC_NBMAX + 1); }  // [warps][2]
+  __host__ __device__ size_t ints() const { return red() + 2 * (GC_THREADS / 32); }  // spiv[nb]
+  __host__ __device__ size_t total() const { return ints() + GC_NBMAX / 2 + 1; }
+};
+
 __global__ void __cluster_dims__(GC_CL, 1, 1) __launch_bounds__(GC_THREADS, 1) gj_cluster_kernel(GcArgs a) {
   extern __shared__ double sm[];
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int item = blockIdx.x / GC_CL;
   const int n = a.n, nb = a.nb, k0 = a.k0, rl = a.rl;
-  const int ldb = nb + 1;                       // odd stride: conflict-free row-wise access
-  constexpr int SL = 2 + 2 * GC_NBMAX;          // slot: best value, best row, candidate row, row cj
-  double* B = sm;                               // rl x ldb  (own rows of the block)
-  double* slots = B + (size_t)rl * ldb;         // [2][SL]  double-buffered per column parity
-  double* prow = slots + 2 * SL;                // scaled pivot row (local)
-  double* drow = prow + GC_NBMAX;               // displaced row cj (local)
-  double* red = drow + GC_NBMAX;                // [warps][2]
-  int* sel = reinterpret_cast<int*>(red + 2 * (GC_THREADS / 32));  // [2]: pr, owner
-  int* spiv = sel + 2;                          // [nb] pivots, written to global at the end
-                                                // (a global store inside the loop would make
-                                                // every cluster barrier's release wait for it)
+  const GcLayout L(rl, nb);
+  const int ldb = L.ldb;
+  constexpr int BOX = GcLayout::BOX;
+  constexpr int CPLD = GC_NBMAX + 1;
+  double* B = sm + L.b();
+  double* box = sm + L.box();
+  double* cjrow = sm + L.cjrow();
+  double* cp = sm + L.cp();
+  double* red = sm + L.red();
+  int* spiv = reinterpret_cast<int*>(sm + L.ints());  // pivots, written to global at the end
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* Mi = a.M.get(item);
   const long long ld = a.M.ld;
   const int r0 = rank * rl;
+  // warp w pushes this CTA's candidate (and row cj when owned) into CTA w's inbox
+  double* peer_box = cluster.map_shared_rank(box, warp);
+  double* peer_cj = cluster.map_shared_rank(cjrow, warp);
 
   for (int e = tid; e < rl * nb; e += GC_THREADS) {
     const int r = e / nb, c = e - r * nb;
@@ -58,11 +93,15 @@ __global__ void __cluster_dims__(GC_CL, 1, 1) __launch_bounds__(GC_THREADS, 1) g
     B[r * ldb + c] = gi < n ? Mi[gi * ld + k0 + c] : 0.0;
   }
   __syncthreads();
+#ifdef GC_PROFILE
+  long long gc_last = clock64();
+#endif
   int flag = 0;
   for (int j = 0; j < nb; ++j) {
     const int cj = k0 + j;
-    double* myslot = slots + (j & 1) * SL;
-    // 1. local candidate among own rows gi >= cj
+    const int j0 = j & ~(GC_SB - 1), j1 = min(nb, j0 + GC_SB);
+    const int par = j & 1;
+    // 1. local candidate among own rows gi >= cj (|value|, ties -> smallest row)
     double best = -1.0;
     int bi = n;
     for (int r = tid; r < rl; r += GC_THREADS) {
@@ -83,7 +122,6 @@ __global__ void __cluster_dims__(GC_CL, 1, 1) __launch_bounds__(GC_THREADS, 1) g
       red[2 * warp + 1] = (double)bi;
     }
     __syncthreads();
-    // every warp reduces the 8 warp results itself (no extra barrier)
     {
       double b = red[0];
       int bix = (int)red[1];
@@ -93,87 +131,108 @@ __global__ void __cluster_dims__(GC_CL, 1, 1) __launch_bounds__(GC_THREADS, 1) g
         const int iw = (int)red[2 * w + 1];
         if (vw > b || (vw == b && iw < bix)) { b = vw; bix = iw; }
       }
-      if (tid == 0) {
-        myslot[0] = b;
-        myslot[1] = (double)bix;
-      }
-      // 2. publish the candidate row and, if owned, the row cj (slots only: B can be
-      //    overwritten right after the single cluster barrier)
-      if (bix < n && bix >= r0 && bix < r0 + rl)
-        for (int c = tid; c < nb; c += GC_THREADS) myslot[2 + c] = B[(bix - r0) * ldb + c];
-      if (cj >= r0 && cj < r0 + rl)
-        for (int c = tid; c < nb; c += GC_THREADS) myslot[2 + GC_NBMAX + c] = B[(cj - r0) * ldb + c];
-    }
-    cluster.sync();  // the only cluster barrier per column
-    // 3. winner over the CL candidates: lanes 0..CL-1 of warp 0 read one remote slot each
-    if (warp == 0) {
-      double vc = -2.0;
-      int ic = n;
-      if (lane < GC_CL) {
-        const double* rs = cluster.map_shared_rank(myslot, lane);
-        vc = rs[0];
-        ic = (int)rs[1];
-      }
-      int oc = lane;
-#pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, vc, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, ic, o);
-        const int oo = __shfl_xor_sync(0xffffffffu, oc, o);
-        if (ov > vc || (ov == vc && oi < ic)) { vc = ov; ic = oi; oc = oo; }
-      }
+      // 2. push: warp w writes {best, row, candidate row} into CTA w's inbox slot [par][rank]
+      double* dst = peer_box + ((size_t)par * GC_CL + rank) * BOX;
       if (lane == 0) {
-        if (ic >= n) ic = -1;  // all NaN: keep the diagonal (row cj)
-        sel[0] = ic;
-        sel[1] = oc;
-        if (!(vc > 0.0)) flag = 1;
+        dst[0] = b;
+        dst[1] = (double)bix;
       }
+      if (bix < n)
+        for (int c = lane; c < nb; c += 32) dst[2 + c] = B[(bix - r0) * ldb + c];
+      if (cj >= r0 && cj < r0 + rl)
+        for (int c = lane; c < nb; c += 32) peer_cj[par * GC_NBMAX + c] = B[(cj - r0) * ldb + c];
     }
-    __syncthreads();
-    int pr = sel[0];
-    const int owner = sel[1];
-    const int owner_cj = cj / rl;
+    GC_T(0);
+    cluster.sync();  // the only cluster barrier per column (release / acquire of the pushes)
+    GC_T(1);
+    // 3. winner from the local inbox (every thread, no further barrier)
+    const double* mybox = box + (size_t)par * GC_CL * BOX;
+    double vb = mybox[0];
+    int pr = (int)mybox[1], owner = 0;
+#pragma unroll
+    for (int c = 1; c < GC_CL; ++c) {
+      const double v = mybox[c * BOX];
+      const int ic = (int)mybox[c * BOX + 1];
+      if (v > vb || (v == vb && ic < pr)) { vb = v; pr = ic; owner = c; }
+    }
+    if (pr >= n) pr = -1;  // all NaN: keep the diagonal (row cj)
+    if (!(vb > 0.0)) flag = 1;
     if (pr < 0) pr = cj;
-    {
-      const double* dsl = cluster.map_shared_rank(myslot, owner_cj) + 2 + GC_NBMAX;
-      const double* psl = cluster.map_shared_rank(myslot, owner) + 2;
-      for (int c = tid; c < nb; c += GC_THREADS) {
-        const double d = dsl[c];
-        drow[c] = d;
-        prow[c] = (pr == cj) ? d : psl[c];
-      }
-    }
+    const double* drow = cjrow + par * GC_NBMAX;
+    const double* prow = (pr == cj) ? drow : mybox + owner * BOX + 2;
     if (tid == 0) spiv[j] = pr;
-    __syncthreads();
+    GC_T(2);
+    // 4. own rows: interchange over all nb columns, elimination over the sub-block only.
+    //    Position cj <- pivot row: sub-block columns scaled (column j <- 1/pivot), the other
+    //    columns keep the unscaled values (their transform is applied at the sub-block end).
     const double inv = 1.0 / prow[j];
-    __syncthreads();
-    for (int c = tid; c < nb; c += GC_THREADS) prow[c] = (c == j) ? inv : prow[c] * inv;
-    __syncthreads();
-    // 4. eliminate own rows: two threads per row, 32 columns each, all loads issued first
-    for (int e = tid; e < 2 * rl; e += GC_THREADS) {
-      const int r = e >> 1, part = e & 1;
+    const int lcj = cj - r0, lpr = pr - r0;
+    for (int c = tid; c < nb; c += GC_THREADS) {
+      const bool insb = c >= j0 && c < j1;
+      const double pc = prow[c];
+      cp[(j - j0) * CPLD + c] = pc;  // C_piv row of this step: the pivot row, other columns
+      if (lcj >= 0 && lcj < rl) B[lcj * ldb + c] = insb ? (c == j ? inv : pc * inv) : pc;
+      if (pr != cj && lpr >= 0 && lpr < rl && !insb) B[lpr * ldb + c] = drow[c];
+    }
+    for (int r = tid; r < rl; r += GC_THREADS) {
       const int gi = r0 + r;
-      if (gi >= n) continue;
+      if (gi >= n || gi == cj) continue;
       double* row = B + r * ldb;
-      const int c0 = part * 32;
-      const double* src = (gi == pr && gi != cj) ? drow : row;
-      double v[32];
+      const bool moved = (gi == pr);  // receives the displaced row cj
+      const double f = moved ? drow[j] : row[j];
 #pragma unroll
-      for (int u = 0; u < 32; ++u) v[u] = (c0 + u < nb) ? src[c0 + u] : 0.0;
-      if (gi == cj) {
-#pragma unroll
-        for (int u = 0; u < 32; ++u)
-          if (c0 + u < nb) row[c0 + u] = prow[c0 + u];
-        continue;
-      }
-      const double f = src[j];
-#pragma unroll
-      for (int u = 0; u < 32; ++u) {
-        const int c = c0 + u;
-        if (c < nb) row[c] = (c == j ? 0.0 : v[u]) - f * prow[c];
+      for (int u = 0; u < GC_SB; ++u) {
+        const int c = j0 + u;
+        if (c < j1) {
+          const double v = moved ? drow[c] : row[c];
+          const double pv = (c == j) ? inv : prow[c] * inv;
+          row[c] = (c == j ? 0.0 : v) - f * pv;
+        }
       }
     }
     __syncthreads();
+    GC_T(3);
+    if (j == j1 - 1 && nb > j1 - j0) {
+      // 5. sub-block end: C <- D C + W C_piv on the other nb - sb columns (local data only: every
+      //    CTA captured the pivot rows from its inbox). One m-tile per warp pass, all n-tiles.
+      const int sb = j1 - j0;
+      const int g = lane >> 2, t = lane & 3;
+      const int mtiles = (rl + 7) >> 3, ocols = nb - sb, ntiles = (ocols + 7) >> 3;
+      const int pr_lo = k0 + j0 - r0, pr_hi = k0 + j1 - r0;  // pivot rows in local numbering
+      for (int mt = warp; mt < mtiles; mt += GC_THREADS / 32) {
+        const int r = mt * 8 + g;
+        const bool rok = r < rl && r0 + r < n;
+        const bool pivrow = r >= pr_lo && r < pr_hi;
+        const double* wrow = B + (size_t)(rok ? r : 0) * ldb + j0;
+        const double a0 = (rok && t < sb) ? wrow[t] : 0.0;
+        const double a1 = (rok && t + 4 < sb) ? wrow[t + 4] : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < GC_NBMAX / 8; ++nt) {
+          if (nt >= ntiles) break;
+          double d[2];
+          int cc[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int x = nt * 8 + 2 * t + h;
+            cc[h] = x < ocols ? (x < j0 ? x : x + sb) : -1;
+            d[h] = (rok && cc[h] >= 0 && !pivrow) ? B[r * ldb + cc[h]] : 0.0;
+          }
+          const int xb = nt * 8 + g;
+          const int cb = xb < ocols ? (xb < j0 ? xb : xb + sb) : -1;
+          const double b0 = (t < sb && cb >= 0) ? cp[t * CPLD + cb] : 0.0;
+          const double b1 = (t + 4 < sb && cb >= 0) ? cp[(t + 4) * CPLD + cb] : 0.0;
+          dmma8x8x4(d[0], d[1], a0, b0);
+          dmma8x8x4(d[0], d[1], a1, b1);
+          if (rok) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (cc[h] >= 0) B[r * ldb + cc[h]] = d[h];
+          }
+        }
+      }
+      __syncthreads();
+      GC_T(4);
+    }
   }
   cluster.sync();
   for (int e = tid; e < rl * nb; e += GC_THREADS) {
@@ -188,8 +247,7 @@ __global__ void __cluster_dims__(GC_CL, 1, 1) __launch_bounds__(GC_THREADS, 1) g
 
 size_t gj_cluster_smem(int n, int nb) {
   const int rl = (n + GC_CL - 1) / GC_CL;
-  return sizeof(double) * ((size_t)rl * (nb + 1) + 2 * (2 + 2 * GC_NBMAX) + 2 * GC_NBMAX + 2 * (GC_THREADS / 32) + 2 +
-                           GC_NBMAX / 2 + 2);
+  return sizeof(double) * GcLayout(rl, nb).total();
 }
 
 // measured faster than the three-level fused path only for n >= ~900 (root and level-1 merges)
@@ -217,3 +275,13 @@ int launch_gj_cluster(int batch, int n, int k0, int nb, MatB M, int* piv, int* s
 }
 
 }  // namespace hps
+
+#ifdef GC_PROFILE
+extern "C" void hps_gc_prof(long long* h, int reset) {
+  cudaMemcpyFromSymbol(h, hps::gc_prof, 8 * sizeof(long long));
+  if (reset) {
+    long long z[8] = {};
+    cudaMemcpyToSymbol(hps::gc_prof, z, sizeof(z));
+  }
+}
+#endif

@@ -67,7 +67,7 @@ def _gj(lib, M, n, ncols):
 
 @pytest.mark.parametrize("n,nrhs,batch", [(1, 0, 2), (5, 3, 4), (15, 90, 3), (33, 7, 2), (60, 240, 5),
                                           (196, 60, 3), (196, 60, 300), (130, 500, 150), (300, 10, 2),
-                                          (900, 124, 1), (1000, 3000, 1)])
+                                          (900, 124, 1), (1000, 3000, 1), (1003, 37, 2), (1920, 200, 1)])
 def test_gj_inverse_matches_numpy(lib, n, nrhs, batch):
     rng = np.random.default_rng(n)
     A = rng.standard_normal((batch, n, n)) + n ** 0.5 * np.eye(n) * rng.choice([-1, 1], size=(batch, 1, 1))
@@ -86,10 +86,10 @@ def test_gj_inverse_matches_numpy(lib, n, nrhs, batch):
     assert int(st.abs().sum()) == 0
 
 
-def test_gj_pivot_sequence_matches_lapack(lib):
+@pytest.mark.parametrize("n", [70, 1000])
+def test_gj_pivot_sequence_matches_lapack(lib, n):
     from scipy.linalg import lu_factor
     rng = np.random.default_rng(3)
-    n = 70
     A = rng.standard_normal((1, n, n))
     M = torch.tensor(A.copy(), device="cuda")
     piv, *_ = _gj(lib, M, n, n)
