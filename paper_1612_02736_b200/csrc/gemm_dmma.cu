@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Batched FP64 GEMM on DMMA tiles (mma.sync.m8n8k4.f64), cp.async double-buffered smem staging.
 //
 //   MODE_GEMM   : C_i = alpha * A_i B_i + beta * C_i            (M x N x K, row-major, any ld)
@@ -129,24 +130,26 @@ __global__ void __launch_bounds__(128) gemm_dmma_kernel(GemmArgs g, int batch_of
 // (8 x 4 DMMA blocks, 64 f64 accumulators / thread), 3-stage cp.async pipeline with 16-byte
 // copies when every operand is 16-byte aligned (else 8-byte copies). Fragment loads use the
 // same conflict-free paddings (A row stride 20, B row stride 132 doubles).
-constexpr int BB_M = 128, BB_K = 16, BB_STAGES = 3;
+constexpr int BB_M = 128, BB_K = 16;
 constexpr int BA_LD = BB_K + 4;
 constexpr int BA_STAGE = BB_M * BA_LD;
-template <int BN> struct BigCfg {
+template <int BN, int STAGES = 3> struct BigCfg {
   static constexpr int THREADS = BN * 2;          // warps = BN / 16, warp tile 64 x 32
   static constexpr int BS_LD = BN + 4;            // = 4 mod 16 doubles
   static constexpr int B_STAGE = BB_K * BS_LD;
-  static constexpr int MINB = BN == 128 ? 1 : 2;  // 128x64 tiles: two CTAs per SM overlap
-  static constexpr size_t SMEM = sizeof(double) * BB_STAGES * (BA_STAGE + B_STAGE);
+  // 128x64 tiles: two CTAs per SM overlap (three with a 2-stage pipeline)
+  static constexpr int MINB = BN == 128 ? 1 : (STAGES == 2 ? 3 : 2);
+  static constexpr size_t SMEM = sizeof(double) * STAGES * (BA_STAGE + B_STAGE);
 };
 
 __device__ __forceinline__ void cp_async16_part(void* smem, const void* gmem, int bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(bytes));
 }
 
-template <int MODE, bool VEC, int BN>
-__global__ void __launch_bounds__(BigCfg<BN>::THREADS, BigCfg<BN>::MINB) gemm_big_kernel(GemmArgs g, int batch_off) {
-  using Cfg = BigCfg<BN>;
+template <int MODE, bool VEC, int BN, int BB_STAGES = 3>
+__global__ void __launch_bounds__(BigCfg<BN, BB_STAGES>::THREADS, BigCfg<BN, BB_STAGES>::MINB)
+    gemm_big_kernel(GemmArgs g, int batch_off) {
+  using Cfg = BigCfg<BN, BB_STAGES>;
   constexpr int NT = Cfg::THREADS;
   constexpr int WN = BN / 32;  // warps along n
   extern __shared__ __align__(16) double gsm[];
@@ -317,37 +320,58 @@ static bool aligned16(const MatB& m) {
   return (p % 16 == 0) && (m.ld % 2 == 0) && (m.stride % 2 == 0);
 }
 
-template <int MODE, int BN>
+template <int MODE, int BN, int ST = 3>
 static void launch_big(const GemmArgs& g, int batch, cudaStream_t s) {
-  using Cfg = BigCfg<BN>;
+  using Cfg = BigCfg<BN, ST>;
   const bool vec = aligned16(g.A) && aligned16(g.B) && aligned16(g.C) &&
                    (MODE != MODE_GJ_UPD || (g.kc % 2 == 0 && g.kb % 2 == 0));
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(gemm_big_kernel<MODE, true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    cudaFuncSetAttribute(gemm_big_kernel<MODE, false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    cudaFuncSetAttribute(gemm_big_kernel<MODE, true, BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Cfg::SMEM);
+    cudaFuncSetAttribute(gemm_big_kernel<MODE, false, BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Cfg::SMEM);
     configured = true;
   }
   const int gx = (g.N + BN - 1) / BN, gy = (g.M + BB_M - 1) / BB_M;
   for (int off = 0; off < batch; off += 65535) {
     dim3 grid(gx, gy, min(65535, batch - off));
     if (vec)
-      gemm_big_kernel<MODE, true, BN><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(g, off);
+      gemm_big_kernel<MODE, true, BN, ST><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(g, off);
     else
-      gemm_big_kernel<MODE, false, BN><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(g, off);
+      gemm_big_kernel<MODE, false, BN, ST><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(g, off);
   }
+}
+
+static int gemm_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HPS_GEMM_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
 }
 
 int launch_gemm(const GemmArgs& g, int batch, int mode, cudaStream_t s) {
   if (batch <= 0 || g.M <= 0 || g.N <= 0) return 0;
-  if (g.M >= 96 && g.N >= 64 && g.K >= 16) {
-    // read-modify-write updates with short K are memory-heavy: 128x64 tiles, 2 CTAs/SM
+  // (N >= 48: the 60-column next-block updates of the p = 32 leaf GJ; the masked tile tail costs
+  // less than the 64x64 kernel's lower efficiency)
+  if (g.M >= 96 && g.N >= 48 && g.K >= 16) {
+    // read-modify-write updates with short K are memory-heavy: 128x64 tiles with a 2-stage
+    // pipeline, 3 CTAs/SM (measured +3 % over 3 stages / 2 CTAs on the K = 64 GJ updates)
     const bool rmw = mode == MODE_GJ_UPD || g.beta != 0.0;
     if (mode == MODE_GEMM) {
-      if (rmw || g.N < 96) launch_big<MODE_GEMM, 64>(g, batch, s);
-      else launch_big<MODE_GEMM, 128>(g, batch, s);
+      if (rmw || g.N < 96) {
+        if (gemm_variant() == 3) launch_big<MODE_GEMM, 64>(g, batch, s);
+        else launch_big<MODE_GEMM, 64, 2>(g, batch, s);
+      } else {
+        launch_big<MODE_GEMM, 128>(g, batch, s);
+      }
     } else {
-      launch_big<MODE_GJ_UPD, 64>(g, batch, s);
+      if (gemm_variant() == 3)
+        launch_big<MODE_GJ_UPD, 64>(g, batch, s);
+      else
+        launch_big<MODE_GJ_UPD, 64, 2>(g, batch, s);
     }
     return cudaGetLastError() == cudaSuccess ? 0 : 2;
   }

@@ -381,7 +381,12 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
     f.col_hi = ncols;
     f.full = 1;
     f.perm_out = perm_out;
-    const int grid = batch < 2 * sms ? batch : 2 * sms;
+    static int per_sm = -1;
+    if (per_sm < 0) {
+      const char* e = getenv("HPS_GJ_FUSED_PER_SM");
+      per_sm = e ? atoi(e) : 2;
+    }
+    const int grid = batch < per_sm * sms ? batch : per_sm * sms;
     return launch_gj_fused(f, grid, s);
   }
   if (anorm) {

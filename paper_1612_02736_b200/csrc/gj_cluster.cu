@@ -97,31 +97,34 @@ __global__ void __cluster_dims__(GC_CL, 1, 1) __launch_bounds__(GC_THREADS, 1) g
   long long gc_last = clock64();
 #endif
   int flag = 0;
+  bool have_cand = false;  // warp candidates for column j already in red (found during elimination)
   for (int j = 0; j < nb; ++j) {
     const int cj = k0 + j;
     const int j0 = j & ~(GC_SB - 1), j1 = min(nb, j0 + GC_SB);
     const int par = j & 1;
     // 1. local candidate among own rows gi >= cj (|value|, ties -> smallest row)
-    double best = -1.0;
-    int bi = n;
-    for (int r = tid; r < rl; r += GC_THREADS) {
-      const int gi = r0 + r;
-      if (gi < n && gi >= cj) {
-        const double v = fabs(B[r * ldb + j]);
-        if (v > best) { best = v; bi = gi; }
+    if (!have_cand) {
+      double best = -1.0;
+      int bi = n;
+      for (int r = tid; r < rl; r += GC_THREADS) {
+        const int gi = r0 + r;
+        if (gi < n && gi >= cj) {
+          const double v = fabs(B[r * ldb + j]);
+          if (v > best) { best = v; bi = gi; }
+        }
       }
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      if (lane == 0) {
+        red[2 * warp] = best;
+        red[2 * warp + 1] = (double)bi;
+      }
+      __syncthreads();
     }
-    if (lane == 0) {
-      red[2 * warp] = best;
-      red[2 * warp + 1] = (double)bi;
-    }
-    __syncthreads();
     {
       double b = red[0];
       int bix = (int)red[1];
@@ -145,16 +148,24 @@ __global__ void __cluster_dims__(GC_CL, 1, 1) __launch_bounds__(GC_THREADS, 1) g
     GC_T(0);
     cluster.sync();  // the only cluster barrier per column (release / acquire of the pushes)
     GC_T(1);
-    // 3. winner from the local inbox (every thread, no further barrier)
+    // 3. winner from the local inbox (every warp: lane c < CL reads candidate c, shuffle reduce)
     const double* mybox = box + (size_t)par * GC_CL * BOX;
-    double vb = mybox[0];
-    int pr = (int)mybox[1], owner = 0;
-#pragma unroll
-    for (int c = 1; c < GC_CL; ++c) {
-      const double v = mybox[c * BOX];
-      const int ic = (int)mybox[c * BOX + 1];
-      if (v > vb || (v == vb && ic < pr)) { vb = v; pr = ic; owner = c; }
+    double vb = -2.0;
+    int pr = n, owner = lane;
+    if (lane < GC_CL) {
+      vb = mybox[lane * BOX];
+      pr = (int)mybox[lane * BOX + 1];
     }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, vb, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, pr, o);
+      const int oo = __shfl_xor_sync(0xffffffffu, owner, o);
+      if (ov > vb || (ov == vb && oi < pr)) { vb = ov; pr = oi; owner = oo; }
+    }
+    vb = __shfl_sync(0xffffffffu, vb, 0);
+    pr = __shfl_sync(0xffffffffu, pr, 0);
+    owner = __shfl_sync(0xffffffffu, owner, 0);
     if (pr >= n) pr = -1;  // all NaN: keep the diagonal (row cj)
     if (!(vb > 0.0)) flag = 1;
     if (pr < 0) pr = cj;
@@ -174,6 +185,10 @@ __global__ void __cluster_dims__(GC_CL, 1, 1) __launch_bounds__(GC_THREADS, 1) g
       if (lcj >= 0 && lcj < rl) B[lcj * ldb + c] = insb ? (c == j ? inv : pc * inv) : pc;
       if (pr != cj && lpr >= 0 && lpr < rl && !insb) B[lpr * ldb + c] = drow[c];
     }
+    // the next column's candidates come out of the same pass when it lies in this sub-block
+    const bool fuse = j + 1 < j1;
+    double nbest = -1.0;
+    int nbi = n;
     for (int r = tid; r < rl; r += GC_THREADS) {
       const int gi = r0 + r;
       if (gi >= n || gi == cj) continue;
@@ -186,10 +201,28 @@ __global__ void __cluster_dims__(GC_CL, 1, 1) __launch_bounds__(GC_THREADS, 1) g
         if (c < j1) {
           const double v = moved ? drow[c] : row[c];
           const double pv = (c == j) ? inv : prow[c] * inv;
-          row[c] = (c == j ? 0.0 : v) - f * pv;
+          const double nv = (c == j ? 0.0 : v) - f * pv;
+          row[c] = nv;
+          if (c == j + 1 && gi > cj && fabs(nv) > nbest) {  // rows below the next pivot position
+            nbest = fabs(nv);
+            nbi = gi;
+          }
         }
       }
     }
+    if (fuse) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, nbest, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, nbi, o);
+        if (ov > nbest || (ov == nbest && oi < nbi)) { nbest = ov; nbi = oi; }
+      }
+      if (lane == 0) {
+        red[2 * warp] = nbest;
+        red[2 * warp + 1] = (double)nbi;
+      }
+    }
+    have_cand = fuse;
     __syncthreads();
     GC_T(3);
     if (j == j1 - 1 && nb > j1 - j0) {

@@ -25,6 +25,18 @@ namespace hps {
 
 constexpr int FU_THREADS = 256;
 
+#ifdef FU_PROFILE
+__device__ long long fu_prof[8];
+#define FU_T(i)                                  \
+  if (threadIdx.x == 0 && blockIdx.x == 0) {     \
+    const long long now = clock64();             \
+    fu_prof[i] += now - fu_last;                 \
+    fu_last = now;                               \
+  }
+#else
+#define FU_T(i)
+#endif
+
 __device__ __forceinline__ double block_max_nan(double v, double* red) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -44,6 +56,8 @@ __device__ double colnorm_block(const double* Mi, long long ld, int n, double* r
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int r = 0;
+    // 16 independent loads in flight per thread (the column sum is latency-bound otherwise)
+#pragma unroll 4
     for (; r + 4 <= n; r += 4) {
       s0 += fabs(Mi[(r + 0) * ld + c]);
       s1 += fabs(Mi[(r + 1) * ld + c]);
@@ -97,6 +111,9 @@ __global__ void __launch_bounds__(NTH, (RPT >= 8 || NTH > 256 ? 1 : 2)) gj_fused
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
 
+#ifdef FU_PROFILE
+  long long fu_last = clock64();
+#endif
   for (int item = blockIdx.x; item < a.batch; item += gridDim.x) {
     double* Mi = a.M.get(item);
     const long long ld = a.M.ld;
@@ -119,6 +136,7 @@ __global__ void __launch_bounds__(NTH, (RPT >= 8 || NTH > 256 ? 1 : 2)) gj_fused
 #pragma unroll
         for (int t = 0; t < KB; ++t) row[r][t] = (i < n && t < kbc) ? src[t] : 0.0;
       }
+      FU_T(0);
       // Column loop with the panel row rotated in registers so the current column is always
       // row[.][0] (the loop body has static register indices and is NOT unrolled: 1/KB the code
       // of a fully unrolled loop, no instruction-cache thrash). One barrier per column: every
@@ -164,14 +182,25 @@ __global__ void __launch_bounds__(NTH, (RPT >= 8 || NTH > 256 ? 1 : 2)) gj_fused
             }
           }
           __syncthreads();
-          double b = slots[0];
-          int pr = (int)slots[1], ws = 0;
-#pragma unroll
-          for (int w = 1; w < FU_THREADS / 32; ++w) {
-            const double vw = slots[w * (KB + 2)];
-            const int iw = (int)slots[w * (KB + 2) + 1];
-            if (vw > b || (vw == b && iw < pr)) { b = vw; pr = iw; ws = w; }
+          // winner over the warp candidates: lane w reads warp w's slot, shuffle reduction
+          // (LAPACK rule), instead of a dependent scan over all slots in every thread
+          constexpr int NWARP = FU_THREADS / 32;
+          double b = -2.0;
+          int pr = n, ws = lane;
+          if (lane < NWARP) {
+            b = slots[lane * (KB + 2)];
+            pr = (int)slots[lane * (KB + 2) + 1];
           }
+#pragma unroll
+          for (int o = NWARP / 2; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, b, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, pr, o);
+            const int ow = __shfl_xor_sync(0xffffffffu, ws, o);
+            if (ov > b || (ov == b && oi < pr)) { b = ov; pr = oi; ws = ow; }
+          }
+          b = __shfl_sync(0xffffffffu, b, 0);
+          pr = __shfl_sync(0xffffffffu, pr, 0);
+          ws = __shfl_sync(0xffffffffu, ws, 0);
           const double* pvr = slots + ws * (KB + 2) + 2;
           if (pr >= n) {  // all candidates NaN: keep the diagonal, NaN propagates
             pr = cj;
@@ -210,6 +239,7 @@ __global__ void __launch_bounds__(NTH, (RPT >= 8 || NTH > 256 ? 1 : 2)) gj_fused
         }
       }
 
+      FU_T(1);
       // ---- 2. factored panel -> shared (column-major) and global; composed interchanges
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
@@ -247,6 +277,7 @@ __global__ void __launch_bounds__(NTH, (RPT >= 8 || NTH > 256 ? 1 : 2)) gj_fused
       }
       __syncthreads();
 
+      FU_T(2);
       // ---- 3./4. other columns of [col_lo, col_hi), chunks of CW
       const int nlog = (a.col_hi - a.col_lo) - kbc;
       const int nm = S.moves[0];
@@ -257,18 +288,33 @@ __global__ void __launch_bounds__(NTH, (RPT >= 8 || NTH > 256 ? 1 : 2)) gj_fused
           if (cc < cw) {
             int pc = a.col_lo + c0 + cc;
             if (pc >= k0) pc += kbc;
-#pragma unroll 8
-            for (int j = 0; j < KB4; ++j) S.W[j * ldw + cc] = (j < kbc) ? Mi[(long long)S.wsrc[j] * ld + pc] : 0.0;
-            for (int mv = 0; mv < nm; ++mv) {
-              const int dst = S.moves[1 + 2 * mv], src = S.moves[2 + 2 * mv];
-              Mi[(long long)dst * ld + pc] = Mi[(long long)src * ld + pc];
+            // W rows via cp.async (no registers, all in flight), then the displaced rows in
+            // groups of 8 loads before their stores. Safe in any grouping: a displaced row
+            // outside the panel always receives an original panel row (a row outside the panel
+            // only ever swaps with the current pivot position), so no source is a destination.
+#pragma unroll
+            for (int j = 0; j < KB4; ++j) {
+              if (j < kbc) cp_async8(&S.W[j * ldw + cc], Mi + (long long)S.wsrc[j] * ld + pc, true);
+              else S.W[j * ldw + cc] = 0.0;
             }
+            cp_async_commit();
+            for (int m0 = 0; m0 < nm; m0 += 8) {
+              double mvv[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (m0 + u < nm) mvv[u] = Mi[(long long)S.moves[2 + 2 * (m0 + u)] * ld + pc];
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (m0 + u < nm) Mi[(long long)S.moves[1 + 2 * (m0 + u)] * ld + pc] = mvv[u];
+            }
+            cp_async_wait<0>();
           } else {
 #pragma unroll
             for (int j = 0; j < KB4; ++j) S.W[j * ldw + cc] = 0.0;
           }
         }
         __syncthreads();
+        FU_T(3);
         const int ntr = (n + 31) >> 5, ntc = (cw + 31) >> 5;
         for (int tile = warp; tile < ntr * ntc; tile += FU_THREADS / 32) {
           const int r0 = (tile / ntc) * 32, cc0 = (tile % ntc) * 32;
@@ -318,10 +364,12 @@ __global__ void __launch_bounds__(NTH, (RPT >= 8 || NTH > 256 ? 1 : 2)) gj_fused
                 if (pcol[jj][h] >= 0) crow[pcol[jj][h]] = acc[i][jj][h];
           }
         }
+        FU_T(4);
       }
     }
     __syncthreads();
     if (tid == 0 && flag && a.status) a.status[item] |= 1;
+    FU_T(5);
 
     if (a.full) {
       // undo the column interchanges of the inverse: inv[:, perm[j]] = M[:, j]
@@ -423,3 +471,13 @@ int launch_gj_fused(const FusedArgs& a, int grid, cudaStream_t s) {
 }
 
 }  // namespace hps
+
+#ifdef FU_PROFILE
+extern "C" void hps_fu_prof(long long* h, int reset) {
+  cudaMemcpyFromSymbol(h, hps::fu_prof, 8 * sizeof(long long));
+  if (reset) {
+    long long z[8] = {};
+    cudaMemcpyToSymbol(hps::fu_prof, z, sizeof(z));
+  }
+}
+#endif
