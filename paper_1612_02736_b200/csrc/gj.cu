@@ -227,7 +227,17 @@ __global__ void colnorm1_kernel(int n, MatB M, unsigned long long* out, int batc
   double s = 0.0;
   if (c < n) {
     const double* Mi = M.get(item);
-    for (int r = 0; r < n; ++r) s += fabs(Mi[(long long)r * M.ld + c]);
+    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int r = 0;
+#pragma unroll 4
+    for (; r + 4 <= n; r += 4) {
+      s += fabs(Mi[(long long)r * M.ld + c]);
+      s1 += fabs(Mi[(long long)(r + 1) * M.ld + c]);
+      s2 += fabs(Mi[(long long)(r + 2) * M.ld + c]);
+      s3 += fabs(Mi[(long long)(r + 3) * M.ld + c]);
+    }
+    for (; r < n; ++r) s += fabs(Mi[(long long)r * M.ld + c]);
+    s = (s + s1) + (s2 + s3);
   }
   __shared__ double red[8];
 #pragma unroll
@@ -366,6 +376,12 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
   const int sms = sm_count();
   const bool fused_full = gj_is_fused_full(batch, n);
   if (fused_full) {
+    // |A|_1 as a separate bandwidth-bound pass: inside the persistent kernel the column sums
+    // were a latency-bound sweep over each matrix (~13 % of its time at n = 196)
+    if (anorm) {
+      const int rc = launch_colnorm1(batch, n, M, anorm, s);
+      if (rc) return rc;
+    }
     FusedArgs f{};
     f.batch = batch;
     f.n = n;
@@ -373,7 +389,7 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
     f.M = M;
     f.piv = piv;
     f.status = status;
-    f.anorm = anorm;
+    f.anorm = nullptr;
     f.ainvnorm = ainvnorm;
     f.k_begin = 0;
     f.k_end = n;

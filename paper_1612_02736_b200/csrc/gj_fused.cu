@@ -137,108 +137,121 @@ __global__ void __launch_bounds__(NTH, (RPT >= 8 || NTH > 256 ? 1 : 2)) gj_fused
         for (int t = 0; t < KB; ++t) row[r][t] = (i < n && t < kbc) ? src[t] : 0.0;
       }
       FU_T(0);
-      // Column loop with the panel row rotated in registers so the current column is always
-      // row[.][0] (the loop body has static register indices and is NOT unrolled: 1/KB the code
-      // of a fully unrolled loop, no instruction-cache thrash). One barrier per column: every
-      // warp publishes its best candidate row (double-buffered slots), every thread then picks
-      // the global winner (LAPACK rule: largest |value|, ties -> smallest row) itself.
+      // composed interchanges of this panel, built by thread 0 as the pivots are chosen
+      for (int x = k0 + tid; x < n; x += FU_THREADS) S.rowid[x] = x;
+      // Column loop with the panel row rotated in registers by 4 columns at a time: the 4
+      // columns of a group use static register indices (row[.][q]), one 4-way rotation per
+      // group brings the next group to the front (KB/4 rotations restore the column order).
+      // One barrier per column: every warp publishes its best candidate row (double-buffered
+      // slots), every warp then picks the global winner (LAPACK rule: largest |value|, ties
+      // -> smallest row) with a shuffle reduction over the warp slots.
+      static_assert(KB % 4 == 0, "panel width must be a multiple of 4");
 #pragma unroll 1
-      for (int j = 0; j < KB; ++j) {
-        if (j < kbc) {
-          const int cj = k0 + j;
-          double* slots = S.slots + (j & 1) * (FU_THREADS / 32) * (KB + 2);
-          double* disp = S.bufB + (j & 1) * KB;
-          double best = -1.0;
-          int bi = n;
+      for (int jb = 0; jb < KB; jb += 4) {
 #pragma unroll
-          for (int r = 0; r < RPT; ++r) {
-            const int i = tid + r * FU_THREADS;
-            if (i < n && i >= cj) {
-              const double v = fabs(row[r][0]);
-              if (v > best) { best = v; bi = i; }
+        for (int q = 0; q < 4; ++q) {
+          const int j = jb + q;
+          if (j < kbc) {
+            const int cj = k0 + j;
+            double* slots = S.slots + (j & 1) * (FU_THREADS / 32) * (KB + 2);
+            double* disp = S.bufB + (j & 1) * KB;
+            double best = -1.0;
+            int bi = n;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+              const int i = tid + r * FU_THREADS;
+              if (i < n && i >= cj) {
+                const double v = fabs(row[r][q]);
+                if (v > best) { best = v; bi = i; }
+              }
             }
-          }
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-          }
-          double* my = slots + warp * (KB + 2);
-          if (lane == 0) {
-            my[0] = best;
-            my[1] = (double)bi;
-          }
-#pragma unroll
-          for (int r = 0; r < RPT; ++r) {
-            const int i = tid + r * FU_THREADS;
-            if (i == bi) {
-#pragma unroll
-              for (int t = 0; t < KB; ++t) my[2 + t] = row[r][t];
+            for (int o = 16; o > 0; o >>= 1) {
+              const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+              const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+              if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
             }
-            if (i == cj) {
-#pragma unroll
-              for (int t = 0; t < KB; ++t) disp[t] = row[r][t];
+            double* my = slots + warp * (KB + 2);
+            if (lane == 0) {
+              my[0] = best;
+              my[1] = (double)bi;
             }
-          }
-          __syncthreads();
-          // winner over the warp candidates: lane w reads warp w's slot, shuffle reduction
-          // (LAPACK rule), instead of a dependent scan over all slots in every thread
-          constexpr int NWARP = FU_THREADS / 32;
-          double b = -2.0;
-          int pr = n, ws = lane;
-          if (lane < NWARP) {
-            b = slots[lane * (KB + 2)];
-            pr = (int)slots[lane * (KB + 2) + 1];
-          }
 #pragma unroll
-          for (int o = NWARP / 2; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, b, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, pr, o);
-            const int ow = __shfl_xor_sync(0xffffffffu, ws, o);
-            if (ov > b || (ov == b && oi < pr)) { b = ov; pr = oi; ws = ow; }
-          }
-          b = __shfl_sync(0xffffffffu, b, 0);
-          pr = __shfl_sync(0xffffffffu, pr, 0);
-          ws = __shfl_sync(0xffffffffu, ws, 0);
-          const double* pvr = slots + ws * (KB + 2) + 2;
-          if (pr >= n) {  // all candidates NaN: keep the diagonal, NaN propagates
-            pr = cj;
-            pvr = disp;
-          }
-          if (tid == 0) {
-            if (!(b > 0.0)) flag = 1;
-            S.spiv[j] = pr;
-            piv[cj] = pr;
-          }
-          const double inv = 1.0 / pvr[0];
+            for (int r = 0; r < RPT; ++r) {
+              const int i = tid + r * FU_THREADS;
+              if (i == bi) {
 #pragma unroll
-          for (int r = 0; r < RPT; ++r) {
-            const int i = tid + r * FU_THREADS;
-            if (i == pr && pr != cj) {
+                for (int t = 0; t < KB; ++t) my[2 + t] = row[r][t];
+              }
+              if (i == cj) {
 #pragma unroll
-              for (int t = 0; t < KB; ++t) row[r][t] = disp[t];
+                for (int t = 0; t < KB; ++t) disp[t] = row[r][t];
+              }
             }
-            if (i == cj) {
+            __syncthreads();
+            // winner over the warp candidates: lane w reads warp w's slot, shuffle reduction
+            constexpr int NWARP = FU_THREADS / 32;
+            double b = -2.0;
+            int pr = n, ws = lane;
+            if (lane < NWARP) {
+              b = slots[lane * (KB + 2)];
+              pr = (int)slots[lane * (KB + 2) + 1];
+            }
 #pragma unroll
-              for (int t = 0; t < KB; ++t) row[r][t] = (t == 0) ? inv : pvr[t] * inv;
-            } else {
-              const double f = row[r][0];
+            for (int o = NWARP / 2; o > 0; o >>= 1) {
+              const double ov = __shfl_xor_sync(0xffffffffu, b, o);
+              const int oi = __shfl_xor_sync(0xffffffffu, pr, o);
+              const int ow = __shfl_xor_sync(0xffffffffu, ws, o);
+              if (ov > b || (ov == b && oi < pr)) { b = ov; pr = oi; ws = ow; }
+            }
+            b = __shfl_sync(0xffffffffu, b, 0);
+            pr = __shfl_sync(0xffffffffu, pr, 0);
+            ws = __shfl_sync(0xffffffffu, ws, 0);
+            const double* pvr = slots + ws * (KB + 2) + 2;
+            if (pr >= n) {  // all candidates NaN: keep the diagonal, NaN propagates
+              pr = cj;
+              pvr = disp;
+            }
+            if (tid == 0) {
+              if (!(b > 0.0)) flag = 1;
+              S.spiv[j] = pr;
+              piv[cj] = pr;
+              const int tr = S.rowid[cj];
+              S.rowid[cj] = S.rowid[pr];
+              S.rowid[pr] = tr;
+            }
+            const double inv = 1.0 / pvr[q];
 #pragma unroll
-              for (int t = 0; t < KB; ++t) row[r][t] = ((t == 0) ? 0.0 : row[r][t]) - f * ((t == 0) ? inv : pvr[t] * inv);
+            for (int r = 0; r < RPT; ++r) {
+              const int i = tid + r * FU_THREADS;
+              if (i == pr && pr != cj) {
+#pragma unroll
+                for (int t = 0; t < KB; ++t) row[r][t] = disp[t];
+              }
+              if (i == cj) {
+#pragma unroll
+                for (int t = 0; t < KB; ++t) row[r][t] = (t == q) ? inv : pvr[t] * inv;
+              } else {
+                const double f = row[r][q];
+#pragma unroll
+                for (int t = 0; t < KB; ++t)
+                  row[r][t] = ((t == q) ? 0.0 : row[r][t]) - f * ((t == q) ? inv : pvr[t] * inv);
+              }
             }
           }
         }
-        // rotate: next column to the front (KB rotations in total restore the column order)
+        // rotate by 4: the next group of columns to the front
 #pragma unroll
         for (int r = 0; r < RPT; ++r) {
-          const double t0 = row[r][0];
+          double t0[4];
 #pragma unroll
-          for (int t = 0; t < KB - 1; ++t) row[r][t] = row[r][t + 1];
-          row[r][KB - 1] = t0;
+          for (int u = 0; u < 4; ++u) t0[u] = row[r][u];
+#pragma unroll
+          for (int t = 0; t < KB - 4; ++t) row[r][t] = row[r][t + 4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) row[r][KB - 4 + u] = t0[u];
         }
       }
-
       FU_T(1);
       // ---- 2. factored panel -> shared (column-major) and global; composed interchanges
 #pragma unroll
@@ -254,26 +267,19 @@ __global__ void __launch_bounds__(NTH, (RPT >= 8 || NTH > 256 ? 1 : 2)) gj_fused
         }
       }
       for (int e = tid; e < (KB4 - KB) * ldp; e += FU_THREADS) S.P[KB * ldp + e] = 0.0;
-      for (int x = k0 + tid; x < n; x += FU_THREADS) S.rowid[x] = x;
       __syncthreads();
-      if (tid == 0) {
-        for (int j = 0; j < kbc; ++j) {
-          const int p = S.spiv[j];
-          const int t = S.rowid[k0 + j];
-          S.rowid[k0 + j] = S.rowid[p];
-          S.rowid[p] = t;
+      if (warp == 0) {
+        // W sources and the displaced rows outside the panel (lane j: pivot step j)
+        const int x = lane < kbc ? S.spiv[lane] : -1;
+        if (lane < kbc) S.wsrc[lane] = S.rowid[k0 + lane];
+        const bool mv = x >= k0 + kbc && S.rowid[x] != x;
+        const unsigned bal = __ballot_sync(0xffffffffu, mv);
+        if (mv) {
+          const int slot = __popc(bal & ((1u << lane) - 1u));
+          S.moves[1 + 2 * slot] = x;
+          S.moves[2 + 2 * slot] = S.rowid[x];
         }
-        int nm = 0;
-        for (int j = 0; j < kbc; ++j) {
-          S.wsrc[j] = S.rowid[k0 + j];
-          const int x = S.spiv[j];
-          if (x >= k0 + kbc && S.rowid[x] != x) {
-            S.moves[1 + 2 * nm] = x;
-            S.moves[2 + 2 * nm] = S.rowid[x];
-            ++nm;
-          }
-        }
-        S.moves[0] = nm;
+        if (lane == 0) S.moves[0] = __popc(bal);
       }
       __syncthreads();
 
