@@ -482,6 +482,24 @@ __global__ void __launch_bounds__(256) sweep_mega_kernel(const SweepStep* steps,
       sweep_unit<NR, false>(a, item, u - item * nch, nch, rows, sm);
       __syncthreads();
     }
+    if (s + 1 < nsteps) {
+      // operators never depend on the sweep data: stream this CTA's units of the next step into
+      // L2 before the grid barrier, so the barrier's latency overlaps the fetch
+      const GemvArgs& b = steps[s + 1].a;
+      const int nch1 = steps[s + 1].nchunks, rows1 = steps[s + 1].rows_per_cta;
+      const int units1 = b.nitems * nch1;
+      for (int u = blockIdx.x; u < units1; u += gridDim.x) {
+        const int item = u / nch1, ch = u - item * nch1;
+        const double* Ai = b.A.get(item);
+        const int r0 = ch * rows1, r1 = min(b.R, r0 + rows1);
+        for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+          const double* rp = Ai + (long long)r * b.A.ld;
+          const uintptr_t lo = reinterpret_cast<uintptr_t>(rp) & ~(uintptr_t)15;
+          const uintptr_t hi = (reinterpret_cast<uintptr_t>(rp + b.K) + 15) & ~(uintptr_t)15;
+          prefetch_l2_bulk(reinterpret_cast<const void*>(lo), (unsigned)(hi - lo));
+        }
+      }
+    }
     grid.sync();
   }
 }
@@ -586,6 +604,16 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
   }
   const size_t smem = sizeof(double) * NR * ((size_t)a.K + (a.mode2 == 2 ? a.R : 0));
   if (smem > 48 * 1024) return false;
+  {
+    // chain steps (one CTA per item, two dependent stages) with too few items to fill the GPU
+    // run as two row-chunked launches instead (HPS_CHAIN_SPLIT: item threshold)
+    static int split = -1;
+    if (split < 0) {
+      const char* e = getenv("HPS_CHAIN_SPLIT");
+      split = e ? atoi(e) : 300;
+    }
+    if (a.mode2 == 2 && a.nitems < split) return false;
+  }
   const int rows = sweep_rows_per_cta(a);
   const int gx = (a.R + rows - 1) / rows;
   static int variant = -1;

@@ -23,6 +23,8 @@ import warnings
 from collections.abc import Mapping
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 import torch
 
@@ -310,7 +312,8 @@ class FactorizedSolver:
         for step in prog["down"]:
             _ext.check(lib.hps_sweep_gemv(step, s), "downward sweep")
 
-    use_mega = False  # single cooperative launch for the parent levels (hps_sweep_program_run); measured slower than graph replay on B200 (r01), opt-in
+    # single cooperative launch for the parent levels (hps_sweep_program_run); opt-in (HPS_SWEEP_MEGA=1)
+    use_mega = os.environ.get("HPS_SWEEP_MEGA", "0") == "1"
 
     def _execute(self, prog, down=True):
         if self.mode == "econ":
