@@ -34,6 +34,9 @@ from .geometry import enumerate_gauss_nodes
 from .spectral import edge_interpolators, shape_constants
 
 RCOND_FLOOR = 1e-13
+# single-RHS split-K only above this many operator bytes (HPS_SPLIT_BYTES)
+_SPLIT_BYTES = float(os.environ.get("HPS_SPLIT_BYTES", "4e6"))
+_SPLIT_CTAS = int(os.environ.get("HPS_SPLIT_CTAS", "600"))  # split-K when a step has fewer CTAs
 BUILD_COUNT = 0
 
 
@@ -442,13 +445,13 @@ class FactorizedSolver:
             K = spec["K"]
             # the single-launch sweep program stages each step's x in 48 KB of shared memory
             must = nrhs <= 2 and K * 8 * nrhs > 40 * 1024
-            if not must and nrhs <= 2 and 8 * spec["nitems"] * spec["R"] * K < 64e6:
+            if not must and nrhs <= 2 and 8 * spec["nitems"] * spec["R"] * K < _SPLIT_BYTES:
                 return [spec]  # single-RHS: the extra reduction step costs more than it saves
             rows_min = 16 if nrhs > 2 else 8
             ctas = spec["nitems"] * -(-spec["R"] // rows_min)
-            if ctas >= 600 and not must:
+            if ctas >= _SPLIT_CTAS and not must:
                 return [spec]
-            want = max(min(-(-600 // ctas), K // 128), -(-K * 8 * nrhs // (40 * 1024)) if must else 1)
+            want = max(min(-(-_SPLIT_CTAS // ctas), K // 128), -(-K * 8 * nrhs // (40 * 1024)) if must else 1)
             ns = min([d for d in range(want, K + 1) if K % d == 0] or [1]) if must else \
                 max([d for d in range(1, want + 1) if K % d == 0] or [1])
             if ns <= 1:
