@@ -27,7 +27,17 @@ namespace hps {
 constexpr int GJ_THREADS = 256;
 // Outer block width of the two-level scheme (inner: fused kernel on the NB-column block;
 // outer: row interchanges + one DMMA GEMM with K = NB over all other columns).
-constexpr int GJ_OUTER_NB = 64;
+constexpr int GJ_OUTER_NB_DEFAULT = 64;
+static int gj_outer_nb() {
+  static int nb = -1;
+  if (nb < 0) {
+    const char* e = getenv("HPS_GJ_NB");
+    nb = e ? atoi(e) : GJ_OUTER_NB_DEFAULT;
+    if (nb < 16) nb = 16;
+    if (nb > 256) nb = 256;
+  }
+  return nb;
+}
 constexpr int GJ_SMEM_BUDGET = 220 * 1024;
 
 static int gj_panel_width(int n) {
@@ -44,7 +54,7 @@ static bool gj_is_fused_full(int batch, int n) { return n <= 256 && (batch >= sm
 
 long long gj_workspace_doubles(int batch, int n, int ncols) {
   if (gj_is_fused_full(batch, n)) return 1;  // the fused kernel needs no global workspace
-  return (long long)batch * GJ_OUTER_NB * ncols + ((long long)batch * n + 1) / 2 + 1;
+  return (long long)batch * gj_outer_nb() * ncols + ((long long)batch * n + 1) / 2 + 1;
 }
 
 __global__ void __launch_bounds__(GJ_THREADS) gj_panel_kernel(int n, int k0, int kb, MatB M, int* piv,
@@ -414,7 +424,7 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
   const bool three_level = batch * ((n + 255) / 256) < 64;
   // equal outer blocks (multiple of 4) so no narrow tail update is left over; many matrices
   // use K = 128 outer updates (half the read-modify-write passes over the trailing columns)
-  const int nbmax = GJ_OUTER_NB;
+  const int nbmax = gj_outer_nb();
   const int nblk = (n + nbmax - 1) / nbmax;
   const int NB = (((n + nblk - 1) / nblk) + 3) & ~3;
   MatB W{wbuf, (long long)NB * ncols, nullptr, ncols, 0};
@@ -455,7 +465,7 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
     }
   }
   // undo the column interchanges of the inverse block (pinv lives in the workspace after W)
-  int* pinv = reinterpret_cast<int*>(wbuf + (size_t)batch * GJ_OUTER_NB * ncols);
+  int* pinv = reinterpret_cast<int*>(wbuf + (size_t)batch * gj_outer_nb() * ncols);
   for (int off = 0; off < batch; off += 65535) {
     const int bb = min(65535, batch - off);
     if (perm_out) {
