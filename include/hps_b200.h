@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define HPS_ABI_VERSION 5
+#define HPS_ABI_VERSION 6
 
 enum hps_status { HPS_OK = 0, HPS_EINVAL = 1, HPS_ECUDA = 2 };
 
@@ -129,11 +129,13 @@ long long hps_merge_workspace_bytes(int npar, int m3, int e);
 int hps_merge_build(const hps_merge_batch* b, void* stream);
 
 /* One batched gather-GEMV of the solve sweeps. pool: rows x nrhs vector arena (RHS fastest).
- *   x_i[k][j] = pool[xidx[i][k]][j] - (x2idx ? pool[x2idx[i][k]][j] : 0)
+ *   x_i[k][j] = pool[xidx[i][k]][j] - (x2idx && x2idx[i][k] >= 0 ? pool[x2idx[i][k]][j] : 0)
  *   y1 = pool[oidx[i][r]][j] = sum_k A_i[r][k] x_i[k][j] + (aidx ? pool[aidx[i][r]][j] : 0)
  * Optional fused second stage (mode2), same launch:
  *   mode2 = 1 (tail):  pool[o2idx[i][r]] = A2_i x_i[K-K2 .. K)          (leaf down, exterior rows)
  *   mode2 = 2 (chain): pool[o2idx[i][r]] = A2_i y1 + pool[a2idx[i][r]]  (parent up: w3 -> h)
+ *   mode2 = 3 (split): pool[o2idx[i][r]] = sum_{k < K2} A_i[r][k] x_i[k]  (R2 = R, aidx null;
+ *                      parent down: u3 = [X | S][d; u_ext] also yields w3 = X d)
  * Output rows must not alias input rows within one call. nrhs <= 16. */
 typedef struct {
   int nitems, R, K, nrhs;

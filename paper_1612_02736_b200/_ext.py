@@ -59,7 +59,7 @@ EXPORTS = ("hps_abi_version", "hps_status_string", "hps_gemm_batched", "hps_gj_w
            "hps_merge_workspace_bytes", "hps_merge_build", "hps_sweep_gemv", "hps_leaf_apply",
            "hps_sweep_program_bytes", "hps_sweep_program_prepare", "hps_sweep_program_run")
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 _lib = None
 _lock = threading.Lock()
 

@@ -201,7 +201,8 @@ static int to_gemv_args(const hps_gemv_batch* gb, GemvArgs* out) {
   a.xstride = a.K;
   a.ostride = a.R;
   if (a.mode2 && (!a.o2idx || a.R2 <= 0 || a.K2 <= 0 || (a.mode2 == 1 && a.K2 > a.K) ||
-                  (a.mode2 == 2 && a.K2 != a.R) || a.mode2 > 2))
+                  (a.mode2 == 2 && a.K2 != a.R) ||
+                  (a.mode2 == 3 && (a.R2 != a.R || a.K2 >= a.K || a.aidx)) || a.mode2 > 3))
     return HPS_EINVAL;
   *out = a;
   return HPS_OK;
@@ -216,7 +217,7 @@ int hps_sweep_program_prepare(const hps_gemv_batch* steps, int nsteps, void* dev
   int rc = HPS_OK;
   for (int i = 0; i < nsteps && rc == HPS_OK; ++i) {
     rc = to_gemv_args(&steps[i], &ga[i]);
-    if (rc == HPS_OK && ga[i].nrhs != ga[0].nrhs) rc = HPS_EINVAL;
+    if (rc == HPS_OK && (ga[i].nrhs != ga[0].nrhs || ga[i].mode2 == 3)) rc = HPS_EINVAL;
   }
   if (rc == HPS_OK) {
     sweep_program_fill(ga, nsteps, ss);
@@ -235,29 +236,9 @@ int hps_sweep_program_run(const void* dev_buffer, int nsteps, int nrhs, long lon
 }
 
 int hps_sweep_gemv(const hps_gemv_batch* gb, void* stream) {
-  if (!gb || !gb->pool || !gb->xidx || !gb->oidx || gb->nrhs < 1 || gb->nrhs > 16) return HPS_EINVAL;
   GemvArgs a{};
-  a.nitems = gb->nitems;
-  a.R = gb->R;
-  a.K = gb->K;
-  a.nrhs = gb->nrhs;
-  a.A = to_matb(&gb->A);
-  a.pool = gb->pool;
-  a.xidx = gb->xidx;
-  a.x2idx = gb->x2idx;
-  a.aidx = gb->aidx;
-  a.oidx = gb->oidx;
-  a.mode2 = gb->mode2;
-  a.R2 = gb->R2;
-  a.K2 = gb->K2;
-  a.A2 = to_matb(&gb->A2);
-  a.a2idx = gb->a2idx;
-  a.o2idx = gb->o2idx;
-  a.xstride = a.K;
-  a.ostride = a.R;
-  if (a.mode2 && (!a.o2idx || a.R2 <= 0 || a.K2 <= 0 || (a.mode2 == 1 && a.K2 > a.K) ||
-                  (a.mode2 == 2 && a.K2 != a.R) || a.mode2 > 2))
-    return HPS_EINVAL;
+  const int rc = to_gemv_args(gb, &a);
+  if (rc != HPS_OK) return rc;
   return launch_gemv_gather(a, (cudaStream_t)stream);
 }
 

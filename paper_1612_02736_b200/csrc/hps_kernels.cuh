@@ -111,6 +111,7 @@ size_t sweep_program_smem(const GemvArgs* steps, int n, int nr);
 void sweep_program_fill(const GemvArgs* steps, int n, SweepStep* out);
 int launch_sweep_program(const SweepStep* dsteps, int n, int nrhs, size_t smem, cudaStream_t s);
 
+
 // Leaf operator application for time stepping (leaf_apply.cu)
 struct LeafApplyArgs {
   int nleaf, p, nrhs;

@@ -46,7 +46,7 @@ static void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
   cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
-// x gather into shared memory: dst[k*ld + j] = pool[xi[k]][j] (- pool[x2[k]][j]) for k < kc,
+// x gather into shared memory: dst[k*ld + j] = pool[xi[k]][j] (- pool[x2[k]][j] if x2[k] >= 0) for k < kc,
 // j < nrhs; zero for kc <= k < kp or j >= nrhs. GU elements per thread are issued together so
 // the index -> value load chains overlap: one memory round trip per GU elements, not per element
 // (the per-element loop left the multi-RHS leaf steps stalled on the gather, r01 ncu).
@@ -108,15 +108,26 @@ __global__ void __launch_bounds__(SW_THREADS) gemv_gather_kernel(GemvArgs a, int
   }
   pdl_wait();
 
-  for (int k0 = 0; k0 < K; k0 += kchunk) {
-    const int kc = min(kchunk, K - k0);
+  // mode2 = 3: chunk boundaries align with K2 and the partial sum over columns [0, K2) is also
+  // stored at o2idx (parent down: u3 = [X | S][d; u_ext] writes w3 = X d on the way)
+  const int ksplit = a.mode2 == 3 ? a.K2 : K;
+  for (int k0 = 0, kc = 0; k0 < K; k0 += kc) {
+    kc = min(kchunk, (k0 < ksplit ? ksplit : K) - k0);
+    if (k0 == ksplit) {
+      __syncthreads();
+      const int* o2 = a.o2idx + (long long)item * a.ostride;
+      for (int e = tid; e < (r1 - r0) * NR; e += SW_THREADS) {
+        const int rr = e / NR, j = e - rr * NR;
+        if (j < nrhs) pool[(long long)o2[r0 + rr] * nrhs + j] = part[e];
+      }
+    }
     __syncthreads();
     for (int e = tid; e < kc * NR; e += SW_THREADS) {
       const int k = e / NR, j = e - k * NR;
       double v = 0.0;
       if (j < nrhs) {
         v = pool[(long long)xi[k0 + k] * nrhs + j];
-        if (x2) v -= pool[(long long)x2[k0 + k] * nrhs + j];
+        if (x2 && x2[k0 + k] >= 0) v -= pool[(long long)x2[k0 + k] * nrhs + j];
       }
       xs[e] = v;
     }
@@ -319,16 +330,51 @@ __global__ void __launch_bounds__(256, 4) gemv_dmma_kernel(GemvArgs a, int rpc, 
 // Staged-x sweep kernel for nrhs <= 2 with an optional fused second stage (tail / chain).
 // Rows are processed by groups of L lanes (L = 4..32 chosen from K so short rows do not idle
 // lanes), 8 independent loads in flight per lane, group-wide shuffle reduction.
+// Scalar accumulation of columns [kb, ke) of RB rows: lane kl of an L-lane group takes columns
+// kb + kl + t*L, U loads per row in flight.
+template <int NR, int RB, int U>
+__device__ __forceinline__ void dot_cols(double (&acc)[RB][NR], const double* const (&row)[RB],
+                                         const bool (&live)[RB], int kb, int ke, int L, int kl,
+                                         const double* xs) {
+  int k = kb + kl;
+  for (; k + (U - 1) * L < ke; k += U * L) {
+    double v[RB][U];
+#pragma unroll
+    for (int q = 0; q < RB; ++q)
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[q][u] = live[q] ? __ldg(row[q] + k + u * L) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        const double xv = xs[(k + u * L) * NR + j];
+#pragma unroll
+        for (int q = 0; q < RB; ++q) acc[q][j] = fma(v[q][u], xv, acc[q][j]);
+      }
+  }
+  for (; k < ke; k += L) {
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+      const double v = live[q] ? __ldg(row[q] + k) : 0.0;
+#pragma unroll
+      for (int j = 0; j < NR; ++j) acc[q][j] = fma(v, xs[k * NR + j], acc[q][j]);
+    }
+  }
+}
+
+// ksplit < K (mode2 = 3): the partial sum over columns [0, ksplit) is also stored at o2idx[r].
 template <int NR, bool VEC, int RB = 2, int U = 4>
 __device__ __forceinline__ void rows_dot(const double* __restrict__ A, long long lda, int R, int r0, int r1,
                                          int K, int L, const double* xs, const int* aidx, const int* oidx,
-                                         double* pool, int nrhs, double* ys) {
+                                         double* pool, int nrhs, double* ys, int ksplit = 1 << 30,
+                                         const int* o2idx = nullptr) {
   // each warp streams RB row groups at once (RB x U independent loads in flight per lane)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = 32 / L, sub = lane / L, kl = lane % L;
   const int nw = blockDim.x >> 5;
+  const bool split = ksplit < K;
   for (int rb = r0 + warp * G * RB; rb < r1; rb += nw * G * RB) {
-    double acc[RB][NR];
+    double acc[RB][NR], accw[RB][NR];
     const double* row[RB];
     bool live[RB];
 #pragma unroll
@@ -337,9 +383,18 @@ __device__ __forceinline__ void rows_dot(const double* __restrict__ A, long long
       live[q] = r < r1;
       row[q] = A + (long long)(live[q] ? r : r0) * lda;
 #pragma unroll
-      for (int j = 0; j < NR; ++j) acc[q][j] = 0.0;
+      for (int j = 0; j < NR; ++j) acc[q][j] = accw[q][j] = 0.0;
     }
-    if (VEC) {
+    if (split) {
+      dot_cols<NR, RB, U>(accw, row, live, 0, ksplit, L, kl, xs);
+      dot_cols<NR, RB, U>(acc, row, live, ksplit, K, L, kl, xs);
+#pragma unroll
+      for (int o = L >> 1; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < RB; ++q)
+#pragma unroll
+          for (int j = 0; j < NR; ++j) accw[q][j] += __shfl_xor_sync(0xffffffffu, accw[q][j], o);
+    } else if (VEC) {
       // 16-byte loads: lane kl covers columns 2kl, 2kl+1 of each 2L-wide strip
       for (int k = 2 * kl; k < K; k += 2 * L * U) {
         double2 v[RB][U];
@@ -367,30 +422,8 @@ __device__ __forceinline__ void rows_dot(const double* __restrict__ A, long long
           }
         }
       }
-    }
-    int k = VEC ? K : kl;
-    for (; k + (U - 1) * L < K; k += U * L) {
-      double v[RB][U];
-#pragma unroll
-      for (int q = 0; q < RB; ++q)
-#pragma unroll
-        for (int u = 0; u < U; ++u) v[q][u] = live[q] ? __ldg(row[q] + k + u * L) : 0.0;
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int j = 0; j < NR; ++j) {
-          const double xv = xs[(k + u * L) * NR + j];
-#pragma unroll
-          for (int q = 0; q < RB; ++q) acc[q][j] = fma(v[q][u], xv, acc[q][j]);
-        }
-    }
-    for (; k < K; k += L) {
-#pragma unroll
-      for (int q = 0; q < RB; ++q) {
-        const double v = live[q] ? __ldg(row[q] + k) : 0.0;
-#pragma unroll
-        for (int j = 0; j < NR; ++j) acc[q][j] = fma(v, xs[k * NR + j], acc[q][j]);
-      }
+    } else {
+      dot_cols<NR, RB, U>(acc, row, live, 0, K, L, kl, xs);
     }
 #pragma unroll
     for (int o = L >> 1; o > 0; o >>= 1)
@@ -407,6 +440,10 @@ __device__ __forceinline__ void rows_dot(const double* __restrict__ A, long long
         for (int j = 0; j < NR; ++j) {
           if (j >= nrhs) break;
           double y = acc[q][j];
+          if (split) {
+            pool[(long long)o2idx[r] * nrhs + j] = accw[q][j];
+            y += accw[q][j];
+          }
           if (aidx) y += pool[(long long)aidx[r] * nrhs + j];
           pool[(long long)oidx[r] * nrhs + j] = y;
           if (ys) ys[(r - r0) * NR + j] = y;
@@ -421,7 +458,7 @@ __host__ __device__ inline int lanes_for(int K) { return K <= 16 ? 4 : (K <= 48 
 // One work unit of a sweep step: item `item`, row chunk `chunk` of `nchunks` (rows_per_cta rows).
 template <int NR, bool VEC, int RB = 2, int U = 4, bool PDL = false>
 __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chunk, int nchunks, int rows_per_cta,
-                                           double* sm) {
+                                           double* sm, int pf_rows = 1 << 30) {
   double* xs = sm;                        // K x NR
   double* ys = xs + (size_t)a.K * NR;     // R x NR (chain mode)
   const int K = a.K, nrhs = a.nrhs;
@@ -431,8 +468,9 @@ __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chun
   const double* Ai = a.A.get(item);
   const int r0 = chunk * rows_per_cta;
   const int r1 = min(a.R, r0 + rows_per_cta);
-  // start streaming this unit's operator rows into L2 while x is gathered
-  for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+  // start streaming this unit's operator rows into L2 while x is gathered (the first pf_rows:
+  // a grid's worth of prefetches must fit in L2 or it evicts rows before they are used)
+  for (int r = r0 + threadIdx.x; r < min(r1, r0 + pf_rows); r += blockDim.x) {
     const double* rp = Ai + (long long)r * a.A.ld;
     const uintptr_t lo = reinterpret_cast<uintptr_t>(rp) & ~(uintptr_t)15;
     const uintptr_t hi = (reinterpret_cast<uintptr_t>(rp + K) + 15) & ~(uintptr_t)15;
@@ -443,7 +481,9 @@ __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chun
   __syncthreads();
   rows_dot<NR, VEC, RB, U>(Ai, a.A.ld, a.R, r0, r1, K, lanes_for(K), xs,
                            a.aidx ? a.aidx + (long long)item * a.ostride : nullptr,
-                           a.oidx + (long long)item * a.ostride, a.pool, nrhs, a.mode2 == 2 ? ys : nullptr);
+                           a.oidx + (long long)item * a.ostride, a.pool, nrhs, a.mode2 == 2 ? ys : nullptr,
+                           a.mode2 == 3 ? a.K2 : 1 << 30,
+                           a.mode2 == 3 ? a.o2idx + (long long)item * a.ostride : nullptr);
   if (a.mode2 == 1) {
     // tail stage rows split evenly over the row chunks of this item
     const int per = (a.R2 + nchunks - 1) / nchunks;
@@ -460,10 +500,10 @@ __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chun
 }
 
 template <int NR, bool VEC, int RB = 2, int U = 4>
-__global__ void __launch_bounds__(256) sweep_kernel(GemvArgs a, int rows_per_cta, int batch_off) {
+__global__ void __launch_bounds__(256) sweep_kernel(GemvArgs a, int rows_per_cta, int batch_off, int pf_rows) {
   extern __shared__ double sm[];
   pdl_trigger();
-  sweep_unit<NR, VEC, RB, U, true>(a, blockIdx.y + batch_off, blockIdx.x, gridDim.x, rows_per_cta, sm);
+  sweep_unit<NR, VEC, RB, U, true>(a, blockIdx.y + batch_off, blockIdx.x, gridDim.x, rows_per_cta, sm, pf_rows);
 }
 
 // Whole solve program in one cooperative launch: the steps run in order, separated by a
@@ -592,6 +632,15 @@ int launch_sweep_program(const SweepStep* dsteps, int n, int nrhs, size_t smem, 
   return err == cudaSuccess ? 0 : 2;
 }
 
+static int variant_of_env() {
+  static int variant = -1;
+  if (variant < 0) {
+    const char* e = getenv("HPS_SWEEP_VARIANT");
+    variant = e ? atoi(e) : 0;
+  }
+  return variant;
+}
+
 template <int NR>
 static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
   {
@@ -600,7 +649,14 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
       const char* e = getenv("HPS_SWEEP_VARIANT");
       old = (e && atoi(e) != 9) ? 0 : 1;  // default: previous gemv_gather kernel for single-stage steps
     }
-    if (old && !a.mode2) return false;  // variant 9: previous gemv_gather kernel
+    // single-stage steps with long rows keep the gemv_gather kernel (HPS_GATHER_MINK: shortest K)
+    static int mink = -1;
+    if (mink < 0) {
+      const char* e = getenv("HPS_GATHER_MINK");
+      mink = e ? atoi(e) : 129;
+    }
+    if (old && a.mode2 == 0 && a.K >= mink) return false;
+    if (old && a.mode2 == 3 && a.K >= mink && getenv("HPS_SPLIT3_GATHER")) return false;
   }
   const size_t smem = sizeof(double) * NR * ((size_t)a.K + (a.mode2 == 2 ? a.R : 0));
   if (smem > 48 * 1024) return false;
@@ -614,21 +670,28 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
     }
     if (a.mode2 == 2 && a.nitems < split) return false;
   }
+  if (a.mode2 == 3 && variant_of_env() != 0 && variant_of_env() != 3) return false;  // split needs the scalar path
   const int rows = sweep_rows_per_cta(a);
   const int gx = (a.R + rows - 1) / rows;
-  static int variant = -1;
-  if (variant < 0) {
-    const char* e = getenv("HPS_SWEEP_VARIANT");
-    variant = e ? atoi(e) : 0;
+  const int variant = variant_of_env();
+  // L2 prefetch per CTA: all rows while a grid's worth (~4 CTAs x 148 SMs) fits in the 126 MB L2,
+  // else the first 16 KB (p = 32 leaves: 588 KB per CTA, full prefetch ran at 4.3 TB/s vs 7.0)
+  static long long pf_kb = -2;
+  if (pf_kb == -2) {
+    const char* e = getenv("HPS_PREFETCH_KB");
+    pf_kb = e ? atoll(e) : -1;
   }
+  const long long cta_bytes = 8LL * a.K * rows;
+  const long long cap = pf_kb >= 0 ? pf_kb * 1024 : (cta_bytes <= 160 * 1024 ? cta_bytes : 16 * 1024);
+  const int pf_rows = (int)(cap / (8LL * a.K));
   for (int off = 0; off < a.nitems; off += 65535) {
     dim3 grid(gx, min(65535, a.nitems - off));
     switch (variant) {
-      case 1: launch_k(sweep_kernel<NR, false, 1, 8>, grid, dim3(256), smem, s, a, rows, off); break;
-      case 2: launch_k(sweep_kernel<NR, true, 1, 4>, grid, dim3(256), smem, s, a, rows, off); break;
-      case 3: launch_k(sweep_kernel<NR, false, 1, 4>, grid, dim3(256), smem, s, a, rows, off); break;
-      case 4: launch_k(sweep_kernel<NR, true, 2, 2>, grid, dim3(256), smem, s, a, rows, off); break;
-      default: launch_k(sweep_kernel<NR, false, 2, 4>, grid, dim3(256), smem, s, a, rows, off); break;
+      case 1: launch_k(sweep_kernel<NR, false, 1, 8>, grid, dim3(256), smem, s, a, rows, off, pf_rows); break;
+      case 2: launch_k(sweep_kernel<NR, true, 1, 4>, grid, dim3(256), smem, s, a, rows, off, pf_rows); break;
+      case 3: launch_k(sweep_kernel<NR, false, 1, 4>, grid, dim3(256), smem, s, a, rows, off, pf_rows); break;
+      case 4: launch_k(sweep_kernel<NR, true, 2, 2>, grid, dim3(256), smem, s, a, rows, off, pf_rows); break;
+      default: launch_k(sweep_kernel<NR, false, 2, 4>, grid, dim3(256), smem, s, a, rows, off, pf_rows); break;
     }
   }
   return true;
@@ -648,7 +711,7 @@ __global__ void __launch_bounds__(256) gemv_row1_kernel(GemvArgs a) {
   double acc = 0.0;
   for (int k = 0; k < a.K; ++k) {
     double v = a.pool[(long long)xi[k] * a.nrhs + j];
-    if (x2) v -= a.pool[(long long)x2[k] * a.nrhs + j];
+    if (x2 && x2[k] >= 0) v -= a.pool[(long long)x2[k] * a.nrhs + j];
     acc = fma(A[k], v, acc);
   }
   const long long o = (long long)a.oidx[(long long)item * a.ostride] * a.nrhs + j;
@@ -668,7 +731,25 @@ int launch_gemv_gather(const GemvArgs& a, cudaStream_t s) {
     if (ok) return cudaGetLastError() == cudaSuccess ? 0 : 2;
   }
   if (a.nrhs > 2 && launch_gemv_tma(a, s)) return cudaGetLastError() == cudaSuccess ? 0 : 2;
-  if (a.mode2) {
+  if (a.mode2 == 3 && a.nrhs > 2) {
+    // split output on the multi-RHS path: w = A[:, :K2] x[:K2] -> o2idx, then
+    // y = A[:, K2:] x[K2:] + w -> oidx (the same operator bytes, two launches)
+    GemvArgs b = a;
+    b.mode2 = 0;
+    b.K = a.K2;
+    b.oidx = a.o2idx;
+    int rc = launch_gemv_gather(b, s);
+    if (rc) return rc;
+    GemvArgs c = a;
+    c.mode2 = 0;
+    c.K = a.K - a.K2;
+    c.A.off += a.K2;
+    c.xidx = a.xidx + a.K2;
+    c.x2idx = a.x2idx ? a.x2idx + a.K2 : nullptr;
+    c.aidx = a.o2idx;
+    return launch_gemv_gather(c, s);
+  }
+  if (a.mode2 && a.mode2 != 3) {
     // second stage for the chunked / multi-RHS paths: separate launch after the first
     GemvArgs b = a;
     b.mode2 = 0;

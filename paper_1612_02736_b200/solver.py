@@ -136,6 +136,7 @@ class _ParentGroup:
     xnorm: torch.Tensor = None
     status: torch.Tensor = None
     perm: torch.Tensor = None  # [npar, m3] column order of X (pivot order)
+    y: torch.Tensor = None     # [npar, e, m3] T_ei X, solve-time operator (FactorizedSolver._prepare)
     wrap: dict = None      # singleton wrapped parent: qd, qu, pu, pd, ec, xsw, tw
 
     @property
@@ -186,7 +187,39 @@ class FactorizedSolver:
                 n += g.wrap["xsw"].numel() * 8 + g.tei.numel() * 8
             else:
                 n += (g.xs.numel() + g.tei.numel()) * 8
+            if g.y is not None:
+                n += g.y.numel() * 8
         return n
+
+    def _prepare(self):
+        """Solve-time operator per parent: Y = T_ei X (e x m3, one batched DMMA GEMM per group).
+
+        The reference's upward step is w3 = X d, h = T_ei w3 + [h_a; h_b] (solver.py:284-286): two
+        dependent GEMVs per parent. With Y the upward step is ONE GEMV, h = Y d + [h_a; h_b], and the
+        downward step reads [X | S] once with x = [d; u_ext], producing u3 = X d + S u_ext and, as its
+        partial sum over the first m3 columns, w3 = X d (solver.py:284,335). Operator bytes streamed
+        per solve are unchanged (X moves from the upward to the downward sweep, Y replaces T_ei); the
+        dependent chain and one launch per level disappear. Built once, on the first solve; the time
+        is kept in prep_seconds (build_seconds covers the reference's build_stage work only)."""
+        todo = [g for g in self.parent_groups if g.y is None]
+        if not todo:
+            return
+        t0 = time.perf_counter()
+        lib = _ext.load()
+        s = _stream_ptr()
+        for grp in todo:
+            m3, e = grp.m3, grp.e
+            if grp.wrap is not None:
+                ldx, xsrc, xstride = m3 + grp.wrap["ec"], grp.wrap["xsw"], 0
+            else:
+                ldx, xsrc, xstride = m3 + e, grp.xs, m3 * (m3 + e)
+            n = len(grp.ids)
+            grp.y = torch.empty((n, e, m3), dtype=torch.float64, device=self.device)
+            _ext.check(lib.hps_gemm_batched(n, e, m3, m3, 1.0, _ext.mat(grp.tei, e * m3, m3),
+                                            _ext.mat(xsrc, xstride, ldx), 0.0, _ext.mat(grp.y, e * m3, m3),
+                                            None, 0, s), "solve operator Y = T_ei X")
+        torch.cuda.synchronize()
+        self.prep_seconds = getattr(self, "prep_seconds", 0.0) + time.perf_counter() - t0
 
     # -- solve stage ------------------------------------------------------------------------
     def _leaf_table(self, g):
@@ -311,6 +344,8 @@ class FactorizedSolver:
         for step in prog["up"]:
             _ext.check(lib.hps_sweep_gemv(step, s), "upward sweep")
         if not down:
+            for step in prog["wonly"]:
+                _ext.check(lib.hps_sweep_gemv(step, s), "upward sweep (w3)")
             return
         for step in prog["down"]:
             _ext.check(lib.hps_sweep_gemv(step, s), "downward sweep")
@@ -347,6 +382,7 @@ class FactorizedSolver:
         prog = self._sweeps.get(nrhs)
         if prog is not None:
             return prog
+        self._prepare()
         lay = self._layout
         keep = []
 
@@ -372,7 +408,12 @@ class FactorizedSolver:
             oidx = np.stack([hslot[n] + np.arange(b) for n in grp.ids])
             up.append(gemv(L, b, m, _ext.mat(grp.h if grp.h is not None else 0, b * m, m), xidx, oidx))
             up[-1]["patch"] = ("h", self.leaf_groups.index(grp))
-        # parents, deepest first: w3 = X (h_b[p3b] - h_a[p3a]); h = T_ei w3 + [h_a[p1a]; h_b[p2b]]
+        # parents, deepest first: h = Y d + [h_a[p1a]; h_b[p2b]], d = h_b[p3b] - h_a[p3a], Y = T_ei X
+        # (solver.py:284-286 with the two GEMVs composed; X's columns are in pivot order, so d is
+        # gathered through perm). w3 = X d is produced by the downward step (mode2 = 3); the
+        # upward-only pass (upward_pass) runs the separate "wonly" steps instead.
+        wonly = []
+        dgather = {}
         for grp in sorted(self.parent_groups, key=lambda g_: -g_.depth):
             m3, e = grp.m3, grp.e
             xw, x2w, ow, ah, oh = [], [], [], [], []
@@ -380,35 +421,30 @@ class FactorizedSolver:
             for slot, nid in enumerate(grp.ids):
                 ca, cb = tree.nodes[nid].children
                 en = plan.node[nid]
-                # X's columns are in pivot order: gather the interface jump by perm
                 xw.append(hslot[cb] + en.pos3_b[xperm[slot]])
                 x2w.append(hslot[ca] + en.pos3_a[xperm[slot]])
                 ow.append(lay["W"] + en.j3)
                 ah.append(np.concatenate([hslot[ca] + en.pos1_a, hslot[cb] + en.pos2_b]))
                 oh.append((lay["hpre"][nid] if grp.wrap is not None else hslot[nid]) + np.arange(e))
             nI = len(grp.ids)
+            xw, x2w, ow = np.stack(xw), np.stack(x2w), np.stack(ow)
+            dgather[id(grp)] = (xw, x2w, ow)
+            up.append(gemv(nI, e, m3, _ext.mat(grp.y, e * m3, m3), xw, np.stack(oh), x2idx=x2w, aidx=np.stack(ah)))
             if grp.wrap is not None:
                 ldx = m3 + grp.wrap["ec"]
-                xmat = _ext.mat(grp.wrap["xsw"], m3 * ldx, ldx)
-            else:
-                xmat = _ext.mat(grp.xs, m3 * (m3 + e), m3 + e)
-            teim = _ext.mat(grp.tei, e * m3, m3)
-            per_item = m3 * m3 + e * m3
-            if nI >= 296 or per_item <= 32768:
-                # one launch: the chained second stage reads w3 from shared memory
-                up.append(gemv(nI, m3, m3, xmat, np.stack(xw), np.stack(ow), x2idx=np.stack(x2w),
-                               mode2=2, R2=e, K2=m3, A2=teim, o2idx=np.stack(oh), a2idx=np.stack(ah)))
-            else:
-                up.append(gemv(nI, m3, m3, xmat, np.stack(xw), np.stack(ow), x2idx=np.stack(x2w)))
-                up.append(gemv(nI, e, m3, teim, np.stack(ow), np.stack(oh), aidx=np.stack(ah)))
-            if grp.wrap is not None:
+                wonly.append(gemv(1, m3, m3, _ext.mat(grp.wrap["xsw"], 0, ldx), xw, ow, x2idx=x2w))
                 nid = grp.ids[0]
                 ec = grp.wrap["ec"]
                 up.append(gemv(1, ec, e, _ext.mat(grp.wrap["qd_dev"], 0, e),
                                (lay["hpre"][nid] + np.arange(e))[None], (hslot[nid] + np.arange(ec))[None]))
-        # downward: parents root first: u[j3] = S u_ext + w[j3]   (solver.py:329-335)
+            else:
+                wonly.append(gemv(nI, m3, m3, _ext.mat(grp.xs, m3 * (m3 + e), m3 + e), xw, ow, x2idx=x2w))
+        # downward: parents root first: u[j3] = [X | S][d; u_ext] = w3 + S u_ext, and w[j3] = w3 as
+        # the partial sum over the first m3 columns (solver.py:284,329-335); x2idx = -1 on the S
+        # part (no difference operand)
         for grp in sorted(self.parent_groups, key=lambda g_: g_.depth):
             m3, e = grp.m3, grp.e
+            xw, x2w, ow = dgather[id(grp)]
             if grp.wrap is not None:
                 nid = grp.ids[0]
                 en = plan.node[nid]
@@ -416,13 +452,17 @@ class FactorizedSolver:
                 ext = lay["U"] + en.ext
                 down.append(gemv(1, e, ec, _ext.mat(grp.wrap["pu_dev"], 0, ec), ext[None],
                                  (lay["U"] + en.wrap.fine)[None]))
-                down.append(gemv(1, m3, ec, _ext.mat(grp.wrap["xsw"], m3 * (m3 + ec), m3 + ec, off=m3),
-                                 ext[None], (lay["U"] + en.j3)[None], aidx=(lay["W"] + en.j3)[None]))
+                xi = np.concatenate([xw, ext[None]], axis=1)
+                x2 = np.concatenate([x2w, np.full((1, ec), -1)], axis=1)
+                down.append(gemv(1, m3, m3 + ec, _ext.mat(grp.wrap["xsw"], 0, m3 + ec), xi,
+                                 (lay["U"] + en.j3)[None], x2idx=x2, mode2=3, R2=m3, K2=m3, o2idx=ow))
                 continue
-            xi = np.stack([lay["U"] + plan.node[n].ext_mergeorder for n in grp.ids])
+            ext = np.stack([lay["U"] + plan.node[n].ext_mergeorder for n in grp.ids])
+            xi = np.concatenate([xw, ext], axis=1)
+            x2 = np.concatenate([x2w, np.full(ext.shape, -1)], axis=1)
             j3 = np.stack([plan.node[n].j3 for n in grp.ids])
-            down.append(gemv(len(grp.ids), m3, e, _ext.mat(grp.xs, m3 * (m3 + e), m3 + e, off=m3), xi,
-                             lay["U"] + j3, aidx=lay["W"] + j3))
+            down.append(gemv(len(grp.ids), m3, m3 + e, _ext.mat(grp.xs, m3 * (m3 + e), m3 + e), xi,
+                             lay["U"] + j3, x2idx=x2, mode2=3, R2=m3, K2=m3, o2idx=ow))
         # leaves: u_c[i_ci] = [F | S] [g; u_ext], fused tail stage u_c[i_ce] = L u_ext  (solver.py:325-327)
         for gi, grp in enumerate(self.leaf_groups):
             L = len(grp.ids)
@@ -440,7 +480,7 @@ class FactorizedSolver:
         scratch = [lay["rows"]]
 
         def split(spec):
-            if spec["mode2"] or spec["K"] < 512:
+            if spec["mode2"] not in (0, 3) or spec["K"] < 512:
                 return [spec]
             K = spec["K"]
             # the single-launch sweep program stages each step's x in 48 KB of shared memory
@@ -452,8 +492,17 @@ class FactorizedSolver:
             if ctas >= _SPLIT_CTAS and not must:
                 return [spec]
             want = max(min(-(-_SPLIT_CTAS // ctas), K // 128), -(-K * 8 * nrhs // (40 * 1024)) if must else 1)
-            ns = min([d for d in range(want, K + 1) if K % d == 0] or [1]) if must else \
-                max([d for d in range(1, want + 1) if K % d == 0] or [1])
+            if spec["mode2"] == 3:
+                # every partial lies on one side of the w3 boundary K2: kc divides K2 and K - K2
+                K2 = spec["K2"]
+                ok = [d for d in range(2, K + 1) if K % d == 0 and K2 % (K // d) == 0]
+                if must:
+                    ok = [d for d in ok if (K // d) * 8 * nrhs <= 40 * 1024]
+                below = [d for d in ok if d <= max(want, 1)]
+                ns = max(below) if below else (min(ok) if ok else 1)
+            else:
+                ns = min([d for d in range(want, K + 1) if K % d == 0] or [1]) if must else \
+                    max([d for d in range(1, want + 1) if K % d == 0] or [1])
             if ns <= 1:
                 return [spec]
             kc = K // ns
@@ -470,19 +519,36 @@ class FactorizedSolver:
             part.update(nitems=n * ns, K=kc, A=_ext.MatBatch(0, 0, ptr_t.data_ptr(), A.ld, 0),
                         xidx=spec["xidx"].reshape(n, ns, kc).reshape(n * ns, kc),
                         x2idx=None if spec["x2idx"] is None else spec["x2idx"].reshape(n * ns, kc),
-                        aidx=None, oidx=scr0 + t[:, None] * R + np.arange(R)[None, :])
+                        aidx=None, oidx=scr0 + t[:, None] * R + np.arange(R)[None, :],
+                        mode2=0, R2=0, K2=0, A2=None, o2idx=None, a2idx=None)
+            ii, rr = np.divmod(np.arange(n * R), R)
+            xred = scr0 + ((ii[:, None] * ns + np.arange(ns)[None, :]) * R + rr[:, None])
+            if spec["mode2"] == 3:
+                # one reduction launch: rows [0, nR) sum all ns partials (u3), rows [nR, 2nR) only
+                # the first K2/kc (w3), through per-row coefficient vectors
+                nx = spec["K2"] // kc
+                coef = torch.zeros((2, ns), dtype=torch.float64, device=self.device)
+                coef[0] = 1.0
+                coef[1, :nx] = 1.0
+                rp = torch.as_tensor(np.repeat([coef[0].data_ptr(), coef[1].data_ptr()], n * R).astype(np.int64),
+                                     device=self.device)
+                keep.extend([coef, rp])
+                red = dict(nitems=2 * n * R, R=1, K=ns, A=_ext.MatBatch(0, 0, rp.data_ptr(), ns, 0),
+                           xidx=np.concatenate([xred, xred]), x2idx=None,
+                           oidx=np.concatenate([spec["oidx"].reshape(n * R, 1), spec["o2idx"].reshape(n * R, 1)]),
+                           aidx=None, mode2=0, R2=0, K2=0, A2=None, o2idx=None, a2idx=None)
+                return [part, red]
             ones = torch.ones(ns, dtype=torch.float64, device=self.device)
             keep.append(ones)
-            ii, rr = np.divmod(np.arange(n * R), R)
             red = dict(nitems=n * R, R=1, K=ns, A=_ext.mat(ones, 0, ns),
-                       xidx=scr0 + ((ii[:, None] * ns + np.arange(ns)[None, :]) * R + rr[:, None]),
-                       x2idx=None, oidx=spec["oidx"].reshape(n * R, 1),
+                       xidx=xred, x2idx=None, oidx=spec["oidx"].reshape(n * R, 1),
                        aidx=None if spec["aidx"] is None else spec["aidx"].reshape(n * R, 1),
                        mode2=0, R2=0, K2=0, A2=None, o2idx=None, a2idx=None)
             return [part, red]
 
         up = [s2 for s1 in up for s2 in split(s1)]
         down = [s2 for s1 in down for s2 in split(s1)]
+        wonly = [s2 for s1 in wonly for s2 in split(s1)]
         # Dirichlet data: rows F of the pool, copied onto the root exterior by a 1x1 "gemv" step
         root_ext = plan.node[tree.root].ext
         f_rows = scratch[0]
@@ -508,23 +574,24 @@ class FactorizedSolver:
 
         patches = [(k, i, s_["patch"]) for k, lst in (("up", up), ("down", down))
                    for i, s_ in enumerate(lst) if "patch" in s_]
+        ng = len(self.leaf_groups)
         up = [build(s_) for s_ in up]
         down = [build(s_) for s_ in down]
+        wonly = [build(s_) for s_ in wonly]
         f_in = pool[f_rows:f_rows + root_ext.size]
         mega = {}
-        ng = len(self.leaf_groups)
         if nrhs <= 2 and self.mode != "econ" and self.use_mega and len(up) > ng:
             # the latency-bound middle (parent levels + the f copy) runs as ONE cooperative
             # launch; the bandwidth-bound leaf steps keep their own full-occupancy launches
             lib = _ext.load()
-            for name, steps in (("full", up[ng:] + down[:-ng]), ("up", up[ng:])):
+            for name, steps in (("full", up[ng:] + down[:-ng]), ("up", up[ng:] + wonly)):
                 arr = (_ext.GemvBatch * len(steps))(*steps)
                 buf = torch.empty(int(lib.hps_sweep_program_bytes(len(steps))), dtype=torch.uint8, device=self.device)
                 smem = _ext.C.c_longlong(0)
                 rc = lib.hps_sweep_program_prepare(arr, len(steps), buf.data_ptr(), _ext.C.byref(smem))
                 if rc == 0 and smem.value <= 48 * 1024:
                     mega[name] = (buf, len(steps), smem.value)
-        prog = {"pool": pool, "up": up, "down": down, "keep": keep, "f_in": f_in, "mega": mega,
+        prog = {"pool": pool, "up": up, "down": down, "wonly": wonly, "keep": keep, "f_in": f_in, "mega": mega,
                 "graph": None, "patches": patches}
         self._sweeps[nrhs] = prog
         return prog
