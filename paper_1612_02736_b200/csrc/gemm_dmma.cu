@@ -368,7 +368,16 @@ int launch_gemm(const GemmArgs& g, int batch, int mode, cudaStream_t s) {
         launch_big<MODE_GEMM, 128>(g, batch, s);
       }
     } else {
-      if (gemm_variant() == 3)
+      // long-K outer updates of the three-level GJ: C traffic is amortised over K >= 128, the
+      // 128 x 128 tile's higher math density wins (HPS_GJ_BIG_K: smallest K for it)
+      static int bigk = -1;
+      if (bigk < 0) {
+        const char* e = getenv("HPS_GJ_BIG_K");
+        bigk = e ? atoi(e) : 1 << 30;
+      }
+      if (g.K >= bigk && g.N >= 96)
+        launch_big<MODE_GJ_UPD, 128>(g, batch, s);
+      else if (gemm_variant() == 3)
         launch_big<MODE_GJ_UPD, 64>(g, batch, s);
       else
         launch_big<MODE_GJ_UPD, 64, 2>(g, batch, s);

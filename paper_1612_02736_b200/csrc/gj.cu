@@ -28,15 +28,38 @@ constexpr int GJ_THREADS = 256;
 // Outer block width of the two-level scheme (inner: fused kernel on the NB-column block;
 // outer: row interchanges + one DMMA GEMM with K = NB over all other columns).
 constexpr int GJ_OUTER_NB_DEFAULT = 64;
-static int gj_outer_nb() {
+// Blocking schemes of the batched inversion:
+//   TWO_LEVEL   fused kernel on a 64-column block (panel + update of the block), then row
+//               interchanges + one K = 64 DMMA GEMM over all other columns;
+//   THREE_FEW   few large matrices (top merges): the block itself is factored by narrow panels
+//               (or one 8-CTA cluster per matrix) with multi-CTA updates, look-ahead on a side stream;
+//   THREE_MANY  many large matrices (p = 32 leaves, 1024 x 900 x 1024): 192-wide outer blocks, each
+//               factored as 64-wide fused panels + K = 64 updates inside the block, then ONE outer
+//               K ~ 180 update of the other columns: a third of the read-modify-write passes over
+//               the 7.4 MB matrices (leaf stage 120 -> 112 ms on the B200).
+enum { GJ_TWO_LEVEL = 0, GJ_THREE_FEW = 1, GJ_THREE_MANY = 2 };
+static int gj_scheme(int batch, int n) {
+  static int many = -1, force3 = -1;
+  if (many < 0) {
+    const char* e = getenv("HPS_GJ_MANY");
+    many = e ? atoi(e) : 1;
+    e = getenv("HPS_GJ_THREE");  // 1: three-level (few-large form) for every blocked inversion
+    force3 = e ? atoi(e) : 0;
+  }
+  if (force3 == 1 || batch * ((n + 255) / 256) < 64) return GJ_THREE_FEW;
+  if (many && n >= 512) return GJ_THREE_MANY;
+  return GJ_TWO_LEVEL;
+}
+static int gj_outer_nb(int batch, int n) {
   static int nb = -1;
   if (nb < 0) {
     const char* e = getenv("HPS_GJ_NB");
-    nb = e ? atoi(e) : GJ_OUTER_NB_DEFAULT;
-    if (nb < 16) nb = 16;
+    nb = e ? atoi(e) : 0;
+    if (nb && nb < 16) nb = 16;
     if (nb > 256) nb = 256;
   }
-  return nb;
+  if (nb) return nb;
+  return gj_scheme(batch, n) == GJ_THREE_MANY ? 192 : GJ_OUTER_NB_DEFAULT;
 }
 constexpr int GJ_SMEM_BUDGET = 220 * 1024;
 
@@ -54,7 +77,7 @@ static bool gj_is_fused_full(int batch, int n) { return n <= 256 && (batch >= sm
 
 long long gj_workspace_doubles(int batch, int n, int ncols) {
   if (gj_is_fused_full(batch, n)) return 1;  // the fused kernel needs no global workspace
-  return (long long)batch * gj_outer_nb() * ncols + ((long long)batch * n + 1) / 2 + 1;
+  return (long long)batch * gj_outer_nb(batch, n) * ncols + ((long long)batch * n + 1) / 2 + 1;
 }
 
 __global__ void __launch_bounds__(GJ_THREADS) gj_panel_kernel(int n, int k0, int kb, MatB M, int* piv,
@@ -349,17 +372,18 @@ struct Lookahead {
 // Factor the NB-column block starting at K0 (pivot columns [K0, K0+nb), columns of the block
 // only): one fused CTA per matrix, or for few large matrices panel-only fused launches plus
 // multi-CTA updates inside the block.
-static int factor_block(int batch, int n, int ncols, int K0, int nb, bool three_level, MatB M, int* piv,
+static int factor_block(int batch, int n, int ncols, int K0, int nb, int scheme, MatB M, int* piv,
                         int* status, MatB W, cudaStream_t s) {
+  const bool three_level = scheme != GJ_TWO_LEVEL;
   int rc;
   static int use_cluster = -1;
   if (use_cluster < 0) {
     const char* e = getenv("HPS_GJ_CLUSTER");
     use_cluster = e ? atoi(e) : 1;
   }
-  if (three_level && use_cluster && gj_cluster_ok(n, nb))
+  if (scheme == GJ_THREE_FEW && use_cluster && gj_cluster_ok(n, nb))
     return launch_gj_cluster(batch, n, K0, nb, M, piv, status, s);
-  const int kin = three_level ? gj_fused_panel_width(n, 0) : nb;
+  const int kin = scheme == GJ_THREE_FEW ? gj_fused_panel_width(n, 0) : (scheme == GJ_THREE_MANY ? 64 : nb);
   for (int k0 = K0; k0 < K0 + nb; k0 += kin) {
     const int kb = min(kin, K0 + nb - k0);
     FusedArgs f{};
@@ -421,10 +445,11 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
   }
   // few large matrices: the inner level is itself split (panel-only fused kernel + multi-CTA
   // update of the block) so the whole GPU works on each block instead of one SM per matrix
-  const bool three_level = batch * ((n + 255) / 256) < 64;
+  const int scheme = gj_scheme(batch, n);
+  const bool three_level = scheme != GJ_TWO_LEVEL;
   // equal outer blocks (multiple of 4) so no narrow tail update is left over; many matrices
   // use K = 128 outer updates (half the read-modify-write passes over the trailing columns)
-  const int nbmax = gj_outer_nb();
+  const int nbmax = gj_outer_nb(batch, n);
   const int nblk = (n + nbmax - 1) / nbmax;
   const int NB = (((n + nblk - 1) / nblk) + 3) & ~3;
   MatB W{wbuf, (long long)NB * ncols, nullptr, ncols, 0};
@@ -438,9 +463,9 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
     const char* e = getenv("HPS_GJ_LOOKAHEAD");
     la_mode = e ? atoi(e) : 1;
   }
-  const bool use_la = la.ok && (la_mode == 2 || (la_mode == 1 && three_level));
+  const bool use_la = la.ok && (la_mode == 2 || (la_mode == 1 && scheme == GJ_THREE_FEW));
   int rc;
-  if ((rc = factor_block(batch, n, ncols, 0, min(NB, n), three_level, M, piv, status, W, s))) return rc;
+  if ((rc = factor_block(batch, n, ncols, 0, min(NB, n), scheme, M, piv, status, W, s))) return rc;
   for (int K0 = 0; K0 < n; K0 += NB) {
     const int nb = min(NB, n - K0);
     const int K1 = K0 + nb;
@@ -451,7 +476,7 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
       if (use_la) {
         cudaEventRecord(la.ev_a, s);
         cudaStreamWaitEvent(la.side, la.ev_a, 0);
-        if ((rc = factor_block(batch, n, ncols, K1, nb1, three_level, M, piv, status, W, la.side))) return rc;
+        if ((rc = factor_block(batch, n, ncols, K1, nb1, scheme, M, piv, status, W, la.side))) return rc;
         cudaEventRecord(la.ev_b, la.side);
       }
     }
@@ -460,12 +485,12 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
     if (nb1 > 0) {
       if (use_la)
         cudaStreamWaitEvent(s, la.ev_b, 0);
-      else if ((rc = factor_block(batch, n, ncols, K1, nb1, three_level, M, piv, status, W, s)))
+      else if ((rc = factor_block(batch, n, ncols, K1, nb1, scheme, M, piv, status, W, s)))
         return rc;
     }
   }
   // undo the column interchanges of the inverse block (pinv lives in the workspace after W)
-  int* pinv = reinterpret_cast<int*>(wbuf + (size_t)batch * gj_outer_nb() * ncols);
+  int* pinv = reinterpret_cast<int*>(wbuf + (size_t)batch * gj_outer_nb(batch, n) * ncols);
   for (int off = 0; off < batch; off += 65535) {
     const int bb = min(65535, batch - off);
     if (perm_out) {

@@ -53,9 +53,14 @@ static void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
 template <int NRP, int GU = 8>
 __device__ __forceinline__ void gather_x(double* dst, int ld, const int* __restrict__ xi,
                                          const int* __restrict__ x2, const double* pool, int nrhs, int kc,
-                                         int kp) {
-  const int tot = kp * NRP, nth = blockDim.x;
-  for (int e0 = threadIdx.x; e0 < tot; e0 += GU * nth) {
+                                         int kp, int tid = -1, int nth = 0) {
+  // (tid, nth): the gathering thread group (default: the whole CTA)
+  if (tid < 0) {
+    tid = threadIdx.x;
+    nth = blockDim.x;
+  }
+  const int tot = kp * NRP;
+  for (int e0 = tid; e0 < tot; e0 += GU * nth) {
     int i1[GU], i2[GU];
 #pragma unroll
     for (int u = 0; u < GU; ++u) {
@@ -367,11 +372,15 @@ template <int NR, bool VEC, int RB = 2, int U = 4>
 __device__ __forceinline__ void rows_dot(const double* __restrict__ A, long long lda, int R, int r0, int r1,
                                          int K, int L, const double* xs, const int* aidx, const int* oidx,
                                          double* pool, int nrhs, double* ys, int ksplit = 1 << 30,
-                                         const int* o2idx = nullptr) {
-  // each warp streams RB row groups at once (RB x U independent loads in flight per lane)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                                         const int* o2idx = nullptr, int warp = -1, int nw = 0) {
+  // each warp streams RB row groups at once (RB x U independent loads in flight per lane);
+  // (warp, nw): this warp's index in the row-processing group (default: the whole CTA)
+  const int lane = threadIdx.x & 31;
+  if (warp < 0) {
+    warp = threadIdx.x >> 5;
+    nw = blockDim.x >> 5;
+  }
   const int G = 32 / L, sub = lane / L, kl = lane % L;
-  const int nw = blockDim.x >> 5;
   const bool split = ksplit < K;
   for (int rb = r0 + warp * G * RB; rb < r1; rb += nw * G * RB) {
     double acc[RB][NR], accw[RB][NR];
@@ -504,6 +513,45 @@ __global__ void __launch_bounds__(256) sweep_kernel(GemvArgs a, int rows_per_cta
   extern __shared__ double sm[];
   pdl_trigger();
   sweep_unit<NR, VEC, RB, U, true>(a, blockIdx.y + batch_off, blockIdx.x, gridDim.x, rows_per_cta, sm, pf_rows);
+}
+
+// Several small items per CTA (deep tree levels: thousands of 15..60-row items): the CTA's warps
+// are split into IPC groups of 256/IPC threads, each group gathers its item's x into its own slice
+// of shared memory (named barrier per group) and streams the item's rows. One wave of CTAs covers
+// the level instead of several waves of one-item CTAs. Single row chunk per item; mode2 0 or 3.
+template <int NR, int IPC>
+__global__ void __launch_bounds__(256) sweep_multi_kernel(GemvArgs a, int batch_off, int pf_rows) {
+  extern __shared__ double sm[];
+  constexpr int GT = 256 / IPC;
+  const int grp = threadIdx.x / GT, gtid = threadIdx.x % GT;
+  const int item = (blockIdx.x + batch_off) * IPC + grp;
+  const int K = a.K, nrhs = a.nrhs;
+  double* xs = sm + (size_t)grp * K * NR;
+  pdl_trigger();
+  const bool live = item < a.nitems;
+  const double* Ai = live ? a.A.get(item) : nullptr;
+  if (live) {
+    for (int r = gtid; r < min(a.R, pf_rows); r += GT) {
+      const double* rp = Ai + (long long)r * a.A.ld;
+      const uintptr_t lo = reinterpret_cast<uintptr_t>(rp) & ~(uintptr_t)15;
+      const uintptr_t hi = (reinterpret_cast<uintptr_t>(rp + K) + 15) & ~(uintptr_t)15;
+      prefetch_l2_bulk(reinterpret_cast<const void*>(lo), (unsigned)(hi - lo));
+    }
+  }
+  pdl_wait();
+  if (!live) return;  // the whole group shares the item
+  const int* xi = a.xidx + (long long)item * a.xstride;
+  const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
+  gather_x<NR>(xs, NR, xi, x2, a.pool, nrhs, K, K, gtid, GT);
+  if (GT == 32)
+    __syncwarp();
+  else
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(GT) : "memory");
+  rows_dot<NR, false>(Ai, a.A.ld, a.R, 0, a.R, K, lanes_for(K), xs,
+                      a.aidx ? a.aidx + (long long)item * a.ostride : nullptr,
+                      a.oidx + (long long)item * a.ostride, a.pool, nrhs, nullptr,
+                      a.mode2 == 3 ? a.K2 : 1 << 30, a.mode2 == 3 ? a.o2idx + (long long)item * a.ostride : nullptr,
+                      gtid >> 5, GT / 32);
 }
 
 // Whole solve program in one cooperative launch: the steps run in order, separated by a
@@ -673,6 +721,38 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
   if (a.mode2 == 3 && variant_of_env() != 0 && variant_of_env() != 3) return false;  // split needs the scalar path
   const int rows = sweep_rows_per_cta(a);
   const int gx = (a.R + rows - 1) / rows;
+  {
+    // deep levels: pack IPC items per CTA while a level still fills ~4 CTAs per SM (HPS_MULTI=0: off)
+    static int multi = -1, min_ctas = 0;
+    if (multi < 0) {
+      const char* e = getenv("HPS_MULTI");
+      multi = e ? atoi(e) : 1;
+      e = getenv("HPS_MULTI_CTAS");
+      min_ctas = e ? atoi(e) : 2 * 148;
+    }
+    int ipc = 1;
+    if (multi && gx == 1 && (a.mode2 == 0 || a.mode2 == 3)) {
+      // next ipc: the level still gives min_ctas CTAs, x fits, and the group's warps cover the
+      // item's rows in at most 4 passes (warps x row groups per warp x 2 rows)
+      while (ipc < 8 && (long long)a.nitems / (2 * ipc) >= min_ctas && smem * 2 * ipc <= 48 * 1024 &&
+             a.R <= (8 / (2 * ipc)) * (32 / lanes_for(a.K)) * 2 * 4)
+        ipc *= 2;
+    }
+    if (ipc > 1) {
+      const long long ctas = (a.nitems + ipc - 1) / ipc;
+      const int pf_rows = 1 << 30;
+      for (long long off = 0; off < ctas; off += 2147483647LL) {
+        const dim3 grid((unsigned)ctas);
+        const size_t sm2 = smem * ipc;
+        switch (ipc) {
+          case 2: launch_k(sweep_multi_kernel<NR, 2>, grid, dim3(256), sm2, s, a, 0, pf_rows); break;
+          case 4: launch_k(sweep_multi_kernel<NR, 4>, grid, dim3(256), sm2, s, a, 0, pf_rows); break;
+          default: launch_k(sweep_multi_kernel<NR, 8>, grid, dim3(256), sm2, s, a, 0, pf_rows); break;
+        }
+      }
+      return true;
+    }
+  }
   const int variant = variant_of_env();
   // L2 prefetch per CTA: all rows while a grid's worth (~4 CTAs x 148 SMs) fits in the 126 MB L2,
   // else the first 16 KB (p = 32 leaves: 588 KB per CTA, full prefetch ran at 4.3 TB/s vs 7.0)
