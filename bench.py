@@ -385,7 +385,8 @@ def run_ours(args, rank, ws):
     e2e_t = max_over_ranks(e2e_t, ws)
     lay = solver._layout
     h2d = 8 * (root_ext.size + g_tab.size)
-    d2h = 8 * lay["rows"]
+    # read back: u | w (2 N_gauss), h_root and the leaf tabulations (n_leaves x p^2)
+    d2h = 8 * (2 * solver.plan.n_gauss + lay["hsize"][tree.root] + solver._n_leaves * p * p)
 
     # ---- CPU baseline: oracle on a bounded sample (rank 0, N=1 only)
     cpu = None

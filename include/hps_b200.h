@@ -152,17 +152,6 @@ typedef struct {
 } hps_gemv_batch;
 int hps_sweep_gemv(const hps_gemv_batch* g, void* stream);
 
-/* A whole solve program (ordered sweep steps, nrhs <= 2) executed by ONE cooperative launch with
- * a grid-wide barrier between steps. prepare: validates the steps and copies their device form
- * into dev_buffer (hps_sweep_program_bytes(nsteps) bytes of device memory, synchronous copy) and
- * reports the dynamic shared memory the run needs; every step's x must fit in 48 KB
- * (K * nrhs * 8 bytes, plus R * nrhs * 8 for chained steps). run: enqueue on `stream`. */
-long long hps_sweep_program_bytes(int nsteps);
-int hps_sweep_program_prepare(const hps_gemv_batch* steps, int nsteps, void* dev_buffer,
-                              long long* smem_bytes);
-int hps_sweep_program_run(const void* dev_buffer, int nsteps, int nrhs, long long smem_bytes,
-                          void* stream);
-
 /* Time-stepping right-hand side on the leaves (timestepping.py:117-167 _RhsContext.apply):
  *   g_l[r][j] = alpha u_l[k_r][j] + beta (A u_l)[k_r][j]   at the interior nodes k_r (i_ci order),
  * A = the collocation operator with coefficient samples coef ([6][nleaf][P]; null if beta = 0).

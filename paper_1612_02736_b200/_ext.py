@@ -56,8 +56,7 @@ class LeafApplyArgs(C.Structure):
 
 EXPORTS = ("hps_abi_version", "hps_status_string", "hps_gemm_batched", "hps_gj_workspace_bytes",
            "hps_gj_invert_batched", "hps_leaf_workspace_bytes", "hps_leaf_build",
-           "hps_merge_workspace_bytes", "hps_merge_build", "hps_sweep_gemv", "hps_leaf_apply",
-           "hps_sweep_program_bytes", "hps_sweep_program_prepare", "hps_sweep_program_run")
+           "hps_merge_workspace_bytes", "hps_merge_build", "hps_sweep_gemv", "hps_leaf_apply")
 
 ABI_VERSION = 6
 _lib = None
@@ -103,11 +102,6 @@ def load(build_if_missing: bool = True):
         lib.hps_merge_build.argtypes = [C.POINTER(MergeBatch), C.c_void_p]
         lib.hps_sweep_gemv.argtypes = [C.POINTER(GemvBatch), C.c_void_p]
         lib.hps_leaf_apply.argtypes = [C.POINTER(LeafApplyArgs), C.c_void_p]
-        lib.hps_sweep_program_bytes.restype = C.c_longlong
-        lib.hps_sweep_program_bytes.argtypes = [C.c_int]
-        lib.hps_sweep_program_prepare.argtypes = [C.POINTER(GemvBatch), C.c_int, C.c_void_p,
-                                                  C.POINTER(C.c_longlong)]
-        lib.hps_sweep_program_run.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_longlong, C.c_void_p]
         for name in EXPORTS:
             getattr(lib, name)
         if lib.hps_abi_version() != ABI_VERSION:

@@ -208,33 +208,6 @@ static int to_gemv_args(const hps_gemv_batch* gb, GemvArgs* out) {
   return HPS_OK;
 }
 
-long long hps_sweep_program_bytes(int nsteps) { return (long long)sizeof(SweepStep) * (nsteps > 0 ? nsteps : 0); }
-
-int hps_sweep_program_prepare(const hps_gemv_batch* steps, int nsteps, void* dev_buffer, long long* smem_bytes) {
-  if (!steps || nsteps <= 0 || !dev_buffer || !smem_bytes) return HPS_EINVAL;
-  GemvArgs* ga = new GemvArgs[nsteps];
-  SweepStep* ss = new SweepStep[nsteps];
-  int rc = HPS_OK;
-  for (int i = 0; i < nsteps && rc == HPS_OK; ++i) {
-    rc = to_gemv_args(&steps[i], &ga[i]);
-    if (rc == HPS_OK && (ga[i].nrhs != ga[0].nrhs || ga[i].mode2 == 3)) rc = HPS_EINVAL;
-  }
-  if (rc == HPS_OK) {
-    sweep_program_fill(ga, nsteps, ss);
-    *smem_bytes = (long long)sweep_program_smem(ga, nsteps, ga[0].nrhs <= 1 ? 1 : 2);
-    if (cudaMemcpy(dev_buffer, ss, sizeof(SweepStep) * nsteps, cudaMemcpyHostToDevice) != cudaSuccess) rc = HPS_ECUDA;
-  }
-  delete[] ga;
-  delete[] ss;
-  return rc;
-}
-
-int hps_sweep_program_run(const void* dev_buffer, int nsteps, int nrhs, long long smem_bytes, void* stream) {
-  if (!dev_buffer || nsteps <= 0 || nrhs < 1 || nrhs > 2) return HPS_EINVAL;
-  return launch_sweep_program((const SweepStep*)dev_buffer, nsteps, nrhs, (size_t)smem_bytes,
-                              (cudaStream_t)stream);
-}
-
 int hps_sweep_gemv(const hps_gemv_batch* gb, void* stream) {
   GemvArgs a{};
   const int rc = to_gemv_args(gb, &a);

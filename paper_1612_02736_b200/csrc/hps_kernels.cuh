@@ -102,16 +102,6 @@ int launch_gemv_gather(const GemvArgs& a, cudaStream_t s);
 // TMA-fed multi-RHS path for large leaf levels (sweep_tma.cu); false = not applicable
 bool launch_gemv_tma(const GemvArgs& a, cudaStream_t s);
 
-// Whole sweep program in one cooperative launch (nrhs <= 2): steps separated by grid barriers.
-struct SweepStep {
-  GemvArgs a;
-  int rows_per_cta, nchunks;
-};
-size_t sweep_program_smem(const GemvArgs* steps, int n, int nr);
-void sweep_program_fill(const GemvArgs* steps, int n, SweepStep* out);
-int launch_sweep_program(const SweepStep* dsteps, int n, int nrhs, size_t smem, cudaStream_t s);
-
-
 // Leaf operator application for time stepping (leaf_apply.cu)
 struct LeafApplyArgs {
   int nleaf, p, nrhs;

@@ -10,12 +10,8 @@
 // Bandwidth-bound: each operator entry is read once per call and used for nrhs FMAs.
 #include <cstdlib>
 
-#include <cooperative_groups.h>
-
 #include "hps_common.cuh"
 #include "hps_kernels.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace hps {
 
@@ -554,44 +550,6 @@ __global__ void __launch_bounds__(256) sweep_multi_kernel(GemvArgs a, int batch_
                       gtid >> 5, GT / 32);
 }
 
-// Whole solve program in one cooperative launch: the steps run in order, separated by a
-// grid-wide barrier; the work units of a step (item x row chunk) are dealt round-robin over
-// the resident CTAs. Removes the per-level launch latency of the ~30 short tree levels.
-template <int NR>
-__global__ void __launch_bounds__(256) sweep_mega_kernel(const SweepStep* steps, int nsteps) {
-  extern __shared__ double sm[];
-  cg::grid_group grid = cg::this_grid();
-  for (int s = 0; s < nsteps; ++s) {
-    const GemvArgs a = steps[s].a;
-    const int nch = steps[s].nchunks, rows = steps[s].rows_per_cta;
-    const int units = a.nitems * nch;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int item = u / nch;
-      sweep_unit<NR, false>(a, item, u - item * nch, nch, rows, sm);
-      __syncthreads();
-    }
-    if (s + 1 < nsteps) {
-      // operators never depend on the sweep data: stream this CTA's units of the next step into
-      // L2 before the grid barrier, so the barrier's latency overlaps the fetch
-      const GemvArgs& b = steps[s + 1].a;
-      const int nch1 = steps[s + 1].nchunks, rows1 = steps[s + 1].rows_per_cta;
-      const int units1 = b.nitems * nch1;
-      for (int u = blockIdx.x; u < units1; u += gridDim.x) {
-        const int item = u / nch1, ch = u - item * nch1;
-        const double* Ai = b.A.get(item);
-        const int r0 = ch * rows1, r1 = min(b.R, r0 + rows1);
-        for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-          const double* rp = Ai + (long long)r * b.A.ld;
-          const uintptr_t lo = reinterpret_cast<uintptr_t>(rp) & ~(uintptr_t)15;
-          const uintptr_t hi = (reinterpret_cast<uintptr_t>(rp + b.K) + 15) & ~(uintptr_t)15;
-          prefetch_l2_bulk(reinterpret_cast<const void*>(lo), (unsigned)(hi - lo));
-        }
-      }
-    }
-    grid.sync();
-  }
-}
-
 static int sweep_ctas_target() { return 4 * 148; }
 
 template <int NR>
@@ -638,6 +596,11 @@ static void launch_dmma(const GemvArgs& a, cudaStream_t s) {
 }
 
 static int sweep_rows_per_cta(const GemvArgs& a) {
+  static int rmax = -1;  // HPS_ROWS_MAX: cap on rows per CTA (tuning)
+  if (rmax < 0) {
+    const char* e = getenv("HPS_ROWS_MAX");
+    rmax = e ? atoi(e) : 0;
+  }
   int rows = a.R;
   if (a.mode2 != 2) {
     const int G = 32 / lanes_for(a.K);
@@ -645,39 +608,9 @@ static int sweep_rows_per_cta(const GemvArgs& a) {
     rows = a.R < 64 ? a.R : 64;
     while (rows > minrows && (long long)a.nitems * ((a.R + rows - 1) / rows) < 4 * 148) rows = (rows + 1) / 2;
     if (rows < minrows) rows = minrows < a.R ? minrows : a.R;
+    if (rmax > 0 && rows > rmax) rows = rmax;
   }
   return rows;
-}
-
-size_t sweep_program_smem(const GemvArgs* steps, int n, int nr) {
-  size_t m = 0;
-  for (int i = 0; i < n; ++i) {
-    const size_t b = sizeof(double) * nr * ((size_t)steps[i].K + (steps[i].mode2 == 2 ? steps[i].R : 0));
-    if (b > m) m = b;
-  }
-  return m;
-}
-
-void sweep_program_fill(const GemvArgs* steps, int n, SweepStep* out) {
-  for (int i = 0; i < n; ++i) {
-    out[i].a = steps[i];
-    out[i].rows_per_cta = sweep_rows_per_cta(steps[i]);
-    out[i].nchunks = (steps[i].R + out[i].rows_per_cta - 1) / out[i].rows_per_cta;
-  }
-}
-
-int launch_sweep_program(const SweepStep* dsteps, int n, int nrhs, size_t smem, cudaStream_t s) {
-  if (nrhs > 2 || smem > 48 * 1024) return 1;
-  void* fn = nrhs == 1 ? (void*)sweep_mega_kernel<1> : (void*)sweep_mega_kernel<2>;
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
-  if (per_sm <= 0) return 1;
-  const int grid = per_sm * sms;
-  void* args[] = {(void*)&dsteps, (void*)&n};
-  const cudaError_t err = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, smem, s);
-  return err == cudaSuccess ? 0 : 2;
 }
 
 static int variant_of_env() {

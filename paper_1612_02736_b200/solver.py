@@ -74,8 +74,8 @@ def _ptr_array(ptrs, dev):
 class LeafSolutions(Mapping):
     """leaf id -> (P,) tabulation, backed by one host array (no per-leaf copies)."""
 
-    def __init__(self, ids, rows, table):
-        self._row = {int(n): int(r) for n, r in zip(ids, rows)}
+    def __init__(self, ids, rows, table, rowmap=None):
+        self._row = rowmap if rowmap is not None else {int(n): int(r) for n, r in zip(ids, rows)}
         self._table = table
 
     def __getitem__(self, nid):
@@ -222,6 +222,13 @@ class FactorizedSolver:
         self.prep_seconds = getattr(self, "prep_seconds", 0.0) + time.perf_counter() - t0
 
     # -- solve stage ------------------------------------------------------------------------
+    def _leaf_view(self, table) -> LeafSolutions:
+        """leaf id -> row of a (n_leaves, .) host table; the id -> row map is built once."""
+        rm = getattr(self, "_leaf_rowmap", None)
+        if rm is None:
+            rm = self._leaf_rowmap = {int(n): r for r, n in enumerate(self._leaf_ids)}
+        return LeafSolutions(None, None, table, rowmap=rm)
+
     def _leaf_table(self, g):
         """(n_leaves, m) interior body-load table in leaf-row order (solver.py:241-253)."""
         if g is None:
@@ -286,6 +293,11 @@ class FactorizedSolver:
         g_rows.copy_(torch.as_tensor(gt, dtype=torch.float64).reshape(-1), non_blocking=False)
         if down:
             prog["f_in"][:, 0].copy_(torch.as_tensor(fv, dtype=torch.float64).reshape(-1))
+        if down and self.use_graphs and self.mode != "econ":
+            st = self._run_overlapped(prog)
+            gtab = gt.detach().cpu().numpy() if isinstance(gt, torch.Tensor) else np.asarray(gt)
+            st.g_tab = self._leaf_view(gtab)
+            return st
         self._execute(prog, down=down)
         # D2H of the result regions only: U|W (contiguous), h_root, leaf tabulations
         uw = pool[:2 * N, 0].cpu().numpy()
@@ -293,12 +305,49 @@ class FactorizedSolver:
         st = SolveState(u=uw[:N], w=uw[N:], tree=self.tree, p=self.p, q=self.q,
                         h_root=pool[rs:rs + lay["hsize"][self.tree.root], 0].cpu().numpy())
         gtab = gt.detach().cpu().numpy() if isinstance(gt, torch.Tensor) else np.asarray(gt)
-        st.g_tab = LeafSolutions(self._leaf_ids, range(nl), gtab)
+        st.g_tab = self._leaf_view(gtab)
         if down:
             uc = pool[lay["UC"]:lay["UC"] + nl * P, 0].cpu().numpy().reshape(nl, P)
-            st.leaf_solutions = LeafSolutions(self._leaf_ids, range(nl), uc)
+            st.leaf_solutions = self._leaf_view(uc)
         else:
             st.scratch = {"g": g}
+        return st
+
+    def _run_overlapped(self, prog) -> SolveState:
+        """Solve with the device->host reads overlapped: the graph replays everything up to the
+        leaf downward step, which then runs as a few leaf-range launches; u, w and h_root are read
+        on a side stream while the leaves compute, and each range's tabulations as soon as it is
+        done (the reads are PCIe-bound: 10 MB at config 2 vs a 0.3 ms leaf step)."""
+        lib = _ext.load()
+        lay, pool = self._layout, prog["pool"]
+        N, P, nl = self.plan.n_gauss, self.p ** 2, self._n_leaves
+        cur = torch.cuda.current_stream()
+        side = prog.get("d2h_stream")
+        if side is None:
+            side = prog["d2h_stream"] = torch.cuda.Stream()
+            prog["d2h_events"] = [torch.cuda.Event() for _ in range(len(prog["leaf_chunks"]) + 1)]
+        evs = prog["d2h_events"]
+        self._graph(prog, "graph_head", leaves_down=False).replay()
+        evs[0].record(cur)
+        s = cur.cuda_stream
+        for i, (gb, _r0, _r1) in enumerate(prog["leaf_chunks"]):
+            _ext.check(lib.hps_sweep_gemv(gb, s), "downward sweep")
+            evs[i + 1].record(cur)
+        rs, hs = lay["hslot"][self.tree.root], lay["hsize"][self.tree.root]
+        uw, hr, uc = np.empty(2 * N), np.empty(hs), np.empty((nl, P))
+        ucf = uc.reshape(-1)
+        uc0 = lay["UC"]
+        side.wait_stream(cur)  # the pool writes of earlier work (f, g uploads) are ordered first
+        with torch.cuda.stream(side):
+            side.wait_event(evs[0])
+            torch.from_numpy(uw).copy_(pool[:2 * N, 0])
+            torch.from_numpy(hr).copy_(pool[rs:rs + hs, 0])
+            for i, (_gb, r0, r1) in enumerate(prog["leaf_chunks"]):
+                side.wait_event(evs[i + 1])
+                torch.from_numpy(ucf[r0 * P:r1 * P]).copy_(pool[uc0 + r0 * P:uc0 + r1 * P, 0])
+        cur.wait_stream(side)  # later work that reuses the pool waits for the reads
+        st = SolveState(u=uw[:N], w=uw[N:], tree=self.tree, p=self.p, q=self.q, h_root=hr)
+        st.leaf_solutions = self._leaf_view(uc)
         return st
 
     def solve_device(self, f: torch.Tensor, g: torch.Tensor) -> dict:
@@ -323,35 +372,38 @@ class FactorizedSolver:
     # -- sweep program ----------------------------------------------------------------------
     use_graphs = True
 
-    def _steps(self, prog, down=True):
-        """Enqueue one solve on the current stream: zero u/w, upward sweep, f, downward sweep."""
+    def _steps(self, prog, down=True, leaves_down=True):
+        """Enqueue one solve on the current stream: zero u/w, upward sweep, f, downward sweep
+        (leaves_down=False: everything but the final leaf step, see _solve_host)."""
         lib = _ext.load()
         pool = prog["pool"]
         N = self.plan.n_gauss
         s = _stream_ptr()
         pool[:2 * N].zero_()
-        mega = prog["mega"].get("full" if down else "up")
-        if mega is not None:
-            ng = len(self.leaf_groups)
-            buf, n, smem = mega
-            for step in prog["up"][:ng]:
-                _ext.check(lib.hps_sweep_gemv(step, s), "upward sweep")
-            _ext.check(lib.hps_sweep_program_run(buf.data_ptr(), n, pool.shape[1], smem, s), "sweep program")
-            if down:
-                for step in prog["down"][-ng:]:
-                    _ext.check(lib.hps_sweep_gemv(step, s), "downward sweep")
-            return
         for step in prog["up"]:
             _ext.check(lib.hps_sweep_gemv(step, s), "upward sweep")
         if not down:
             for step in prog["wonly"]:
                 _ext.check(lib.hps_sweep_gemv(step, s), "upward sweep (w3)")
             return
-        for step in prog["down"]:
+        down_steps = prog["down"] if leaves_down else prog["down"][:-len(self.leaf_groups)]
+        for step in down_steps:
             _ext.check(lib.hps_sweep_gemv(step, s), "downward sweep")
 
-    # single cooperative launch for the parent levels (hps_sweep_program_run); opt-in (HPS_SWEEP_MEGA=1)
-    use_mega = os.environ.get("HPS_SWEEP_MEGA", "0") == "1"
+    def _graph(self, prog, key, **kw):
+        """CUDA graph of _steps(prog, **kw), captured on first use."""
+        g = prog.get(key)
+        if g is None:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                self._steps(prog, **kw)
+            torch.cuda.current_stream().wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._steps(prog, **kw)
+            prog[key] = g
+        return g
 
     def _execute(self, prog, down=True):
         if self.mode == "econ":
@@ -366,17 +418,7 @@ class FactorizedSolver:
         if not (down and self.use_graphs):
             self._steps(prog, down)
             return
-        if prog.get("graph") is None:
-            side = torch.cuda.Stream()
-            side.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(side):
-                self._steps(prog)
-            torch.cuda.current_stream().wait_stream(side)
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
-                self._steps(prog)
-            prog["graph"] = graph
-        prog["graph"].replay()
+        self._graph(prog, "graph").replay()
 
     def _program(self, nrhs):
         prog = self._sweeps.get(nrhs)
@@ -577,21 +619,27 @@ class FactorizedSolver:
         ng = len(self.leaf_groups)
         up = [build(s_) for s_ in up]
         down = [build(s_) for s_ in down]
+        # leaf downward step as leaf-range launches (host-API path, _run_overlapped)
+        leaf_chunks = []
+        for gi, grp in enumerate(self.leaf_groups):
+            gb = down[len(down) - ng + gi]
+            L = len(grp.ids)
+            nch = 4 if L >= 4 * 148 else 1
+            for c in range(nch):
+                i0, i1 = L * c // nch, L * (c + 1) // nch
+                cb = _ext.GemvBatch.from_buffer_copy(gb)
+                cb.nitems = i1 - i0
+                if gb.A.base:
+                    cb.A.base = gb.A.base + 8 * i0 * gb.A.stride
+                cb.xidx = gb.xidx + 4 * i0 * gb.K
+                cb.oidx = gb.oidx + 4 * i0 * gb.R
+                if gb.o2idx:
+                    cb.o2idx = gb.o2idx + 4 * i0 * gb.R2
+                leaf_chunks.append((cb, grp.first_row + i0, grp.first_row + i1))
         wonly = [build(s_) for s_ in wonly]
         f_in = pool[f_rows:f_rows + root_ext.size]
-        mega = {}
-        if nrhs <= 2 and self.mode != "econ" and self.use_mega and len(up) > ng:
-            # the latency-bound middle (parent levels + the f copy) runs as ONE cooperative
-            # launch; the bandwidth-bound leaf steps keep their own full-occupancy launches
-            lib = _ext.load()
-            for name, steps in (("full", up[ng:] + down[:-ng]), ("up", up[ng:] + wonly)):
-                arr = (_ext.GemvBatch * len(steps))(*steps)
-                buf = torch.empty(int(lib.hps_sweep_program_bytes(len(steps))), dtype=torch.uint8, device=self.device)
-                smem = _ext.C.c_longlong(0)
-                rc = lib.hps_sweep_program_prepare(arr, len(steps), buf.data_ptr(), _ext.C.byref(smem))
-                if rc == 0 and smem.value <= 48 * 1024:
-                    mega[name] = (buf, len(steps), smem.value)
-        prog = {"pool": pool, "up": up, "down": down, "wonly": wonly, "keep": keep, "f_in": f_in, "mega": mega,
+        prog = {"pool": pool, "up": up, "down": down, "wonly": wonly, "keep": keep, "f_in": f_in,
+                "leaf_chunks": leaf_chunks,
                 "graph": None, "patches": patches}
         self._sweeps[nrhs] = prog
         return prog

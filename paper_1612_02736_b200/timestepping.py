@@ -24,7 +24,7 @@ from . import _ext
 from . import coeffs as coeff_mod
 from . import solver as solver_mod
 from .model import CoefficientField, ProblemSpec
-from .solver import FactorizedSolver, LeafSolutions, SolveState
+from .solver import FactorizedSolver, SolveState
 
 
 @dataclass(frozen=True)
@@ -237,7 +237,7 @@ def _snapshot(solver: FactorizedSolver, stepper: DeviceStepper, j: int = 0) -> S
     uw = pool[:2 * N, j].cpu().numpy()
     uc = pool[lay["UC"]:lay["UC"] + nl * P, j].cpu().numpy().reshape(nl, P)
     st = SolveState(u=uw[:N].copy(), w=uw[N:].copy(), tree=solver.tree, p=solver.p, q=solver.q)
-    st.leaf_solutions = LeafSolutions(solver._leaf_ids, range(nl), uc)
+    st.leaf_solutions = solver._leaf_view(uc)
     return st
 
 
@@ -259,7 +259,7 @@ def cn_run(problem: ParabolicProblem, tree, config: TimeStepConfig, p: int, q: i
     if 0 in record:
         st0 = SolveState(u=np.full(solver.plan.n_gauss, np.nan), w=np.zeros(solver.plan.n_gauss),
                          tree=tree, p=p, q=q)
-        st0.leaf_solutions = LeafSolutions(solver._leaf_ids, range(solver._n_leaves), u0.copy())
+        st0.leaf_solutions = solver._leaf_view(u0.copy())
         states[0.0] = st0
     for step in range(1, config.steps + 1):
         t_next = step * config.k

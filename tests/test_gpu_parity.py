@@ -200,18 +200,26 @@ class TestEconomyMode:
             build_stage(build_uniform_tree(UNIT, 1), catalog("laplace"), 9, 8, mode="compressed")
 
 
-def test_cooperative_sweep_program_matches_graph_path():
+@pytest.mark.parametrize("n", [8, 32])
+def test_overlapped_host_path_matches_eager_program(n):
+    """The host-API path (graph up to the leaf step, leaf-range launches, reads overlapped on a
+    side stream) gives bit-identical results to the eager one-launch-per-step program; n = 32
+    gives 1024 leaves, i.e. 4 leaf ranges."""
     spec = catalog("varcoef_helmholtz", kappa=10.0)
-    tree = build_uniform_tree(UNIT, 8)
+    tree = build_uniform_tree(UNIT, n)
     a = build_stage(tree, spec, 12, 11)
-    b = build_stage(tree, spec, 12, 11)
-    b.use_mega = True
     f = lambda pts: np.sin(2 * pts[:, 0] + pts[:, 1])
-    sa, sb = a.solve(f=f), b.solve(f=f)
-    assert b._program(1)["mega"], "cooperative program was not prepared"
-    assert rel_maxdiff(sb.u, sa.u) <= 1e-14
-    for nid in sa.leaf_solutions:
-        np.testing.assert_allclose(sb.leaf_solutions[nid], sa.leaf_solutions[nid], rtol=0, atol=1e-13)
+    g = lambda pts: np.cos(3 * pts[:, 0]) * pts[:, 1]
+    sa = a.solve(f=f, g=g)
+    assert len(a._program(1)["leaf_chunks"]) == (4 if n * n >= 4 * 148 else 1)
+    a.use_graphs = False
+    sb = a.solve(f=f, g=g)
+    np.testing.assert_array_equal(sa.u, sb.u)
+    np.testing.assert_array_equal(sa.w, sb.w)
+    np.testing.assert_array_equal(sa.h_root, sb.h_root)
+    for nid in sb.leaf_solutions:
+        np.testing.assert_array_equal(sa.leaf_solutions[nid], sb.leaf_solutions[nid])
+        np.testing.assert_array_equal(sa.g_tab[nid], sb.g_tab[nid])
 
 
 class TestUnionDomains:
