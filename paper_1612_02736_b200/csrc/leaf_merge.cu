@@ -13,7 +13,9 @@ namespace hps {
 //   D1 = [i2==j2] dx[i1,j1],    D2 = [i1==j1] dy[i2,j2].
 // The accumulation order matches the reference term by term. A_ii goes to the first m
 // columns of the GJ workspace row, A_ie to its own buffer (multiplied by the lift next).
-constexpr int ASM_ROWS = 8;
+// rows per CTA: the four p x p 1D operators staged in shared memory are amortised over ASM_ROWS
+// rows of output (8 rows read 32 KB of constants per 64 KB written at p = 32)
+constexpr int ASM_ROWS = 32;
 
 __global__ void __launch_bounds__(256) leaf_assemble_kernel(LeafAsmArgs a, int batch_off) {
   extern __shared__ double sd[];
