@@ -334,20 +334,26 @@ class FactorizedSolver:
             _ext.check(lib.hps_sweep_gemv(gb, s), "downward sweep")
             evs[i + 1].record(cur)
         rs, hs = lay["hslot"][self.tree.root], lay["hsize"][self.tree.root]
-        uw, hr, uc = np.empty(2 * N), np.empty(hs), np.empty((nl, P))
-        ucf = uc.reshape(-1)
+        # results land in page-locked host blocks (torch's caching host allocator: a block is
+        # reused once the state holding it is dropped), 3x the pageable read bandwidth here; the
+        # returned arrays are numpy views that keep their block alive
+        uw = torch.empty(2 * N, dtype=torch.float64, pin_memory=True)
+        hr = torch.empty(hs, dtype=torch.float64, pin_memory=True)
+        uc = torch.empty(nl * P, dtype=torch.float64, pin_memory=True)
         uc0 = lay["UC"]
         side.wait_stream(cur)  # the pool writes of earlier work (f, g uploads) are ordered first
         with torch.cuda.stream(side):
             side.wait_event(evs[0])
-            torch.from_numpy(uw).copy_(pool[:2 * N, 0])
-            torch.from_numpy(hr).copy_(pool[rs:rs + hs, 0])
+            uw.copy_(pool[:2 * N, 0], non_blocking=True)
+            hr.copy_(pool[rs:rs + hs, 0], non_blocking=True)
             for i, (_gb, r0, r1) in enumerate(prog["leaf_chunks"]):
                 side.wait_event(evs[i + 1])
-                torch.from_numpy(ucf[r0 * P:r1 * P]).copy_(pool[uc0 + r0 * P:uc0 + r1 * P, 0])
+                uc[r0 * P:r1 * P].copy_(pool[uc0 + r0 * P:uc0 + r1 * P, 0], non_blocking=True)
         cur.wait_stream(side)  # later work that reuses the pool waits for the reads
-        st = SolveState(u=uw[:N], w=uw[N:], tree=self.tree, p=self.p, q=self.q, h_root=hr)
-        st.leaf_solutions = self._leaf_view(uc)
+        side.synchronize()
+        uwn = uw.numpy()
+        st = SolveState(u=uwn[:N], w=uwn[N:], tree=self.tree, p=self.p, q=self.q, h_root=hr.numpy())
+        st.leaf_solutions = self._leaf_view(uc.numpy().reshape(nl, P))
         return st
 
     def solve_device(self, f: torch.Tensor, g: torch.Tensor) -> dict:

@@ -58,4 +58,4 @@ pr.enable()
 for _ in range(20):
     solver.solve(f=f, g=g)
 pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(12)
+pstats.Stats(pr).sort_stats("tottime").print_stats(18)
