@@ -63,7 +63,7 @@ static int gj_outer_nb(int batch, int n) {
   if (sc == GJ_THREE_MANY) return 192;
   // few matrices too small for the cluster panel kernel (n <= 768, e.g. 8-16 merges of m3 = 480):
   // wider outer blocks, fewer read-modify-write passes (config 5 levels 3-4: 4.7 -> 4.4 ms)
-  if (sc == GJ_THREE_FEW && n <= 768 && n >= 384) return 96;
+  if (sc == GJ_THREE_FEW && n <= 768 && n >= 384 && batch > 8) return 96;
   return GJ_OUTER_NB_DEFAULT;
 }
 constexpr int GJ_SMEM_BUDGET = 220 * 1024;
@@ -386,7 +386,9 @@ static int factor_block(int batch, int n, int ncols, int K0, int nb, int scheme,
     const char* e = getenv("HPS_GJ_CLUSTER");
     use_cluster = e ? atoi(e) : 1;
   }
-  if (scheme == GJ_THREE_FEW && use_cluster && gj_cluster_ok(n, nb))
+  // the 8-CTA cluster panel: large n, or medium n (>= 384) with at most 8 matrices (config 5
+  // level 3: 4.54 -> 4.23 ms; with 16 matrices the fused panels win)
+  if (scheme == GJ_THREE_FEW && use_cluster && (n > 768 || batch <= 8) && gj_cluster_ok(n, nb))
     return launch_gj_cluster(batch, n, K0, nb, M, piv, status, s);
   const int kin = scheme == GJ_THREE_FEW ? gj_fused_panel_width(n, 0) : (scheme == GJ_THREE_MANY ? 64 : nb);
   for (int k0 = K0; k0 < K0 + nb; k0 += kin) {

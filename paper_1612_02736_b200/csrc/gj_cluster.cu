@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Block factorisation for FEW LARGE matrices (top-of-tree merges): one thread-block cluster of
 // CL CTAs per matrix holds the n x nb column block in distributed shared memory (CTA c owns rows
 // [c*rl, (c+1)*rl)), and runs Gauss-Jordan with partial pivoting column by column:
@@ -284,7 +285,14 @@ size_t gj_cluster_smem(int n, int nb) {
 }
 
 // measured faster than the three-level fused path only for n >= ~900 (root and level-1 merges)
-bool gj_cluster_ok(int n, int nb) { return n > 768 && nb <= GC_NBMAX && gj_cluster_smem(n, nb) <= 200 * 1024; }
+bool gj_cluster_ok(int n, int nb) {
+  static int nmin = -1;  // HPS_GJ_CLUSTER_NMIN: smallest n for the cluster panel kernel
+  if (nmin < 0) {
+    const char* e = getenv("HPS_GJ_CLUSTER_NMIN");
+    nmin = e ? atoi(e) : 384;
+  }
+  return n >= nmin && nb <= GC_NBMAX && gj_cluster_smem(n, nb) <= 200 * 1024;
+}
 
 int launch_gj_cluster(int batch, int n, int k0, int nb, MatB M, int* piv, int* status, cudaStream_t s) {
   if (!gj_cluster_ok(n, nb)) return 1;
