@@ -159,8 +159,13 @@ def dist_init():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if ws > 1:
+        import torch
         import torch.distributed as dist
-        dist.init_process_group("nccl" if os.environ.get("HPS_BENCH_BACKEND", "nccl") == "nccl" else "gloo")
+        backend = "nccl" if os.environ.get("HPS_BENCH_BACKEND", "nccl") == "nccl" else "gloo"
+        if backend == "nccl":
+            # one process per GPU: bind the device before the group so NCCL uses it
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group(backend)
     return rank, ws
 
 
@@ -174,7 +179,10 @@ def max_over_ranks(x, ws):
 def barrier(ws):
     if ws > 1:
         import torch.distributed as dist
-        dist.barrier()
+        if dist.get_backend() == "nccl":
+            dist.barrier(device_ids=[int(os.environ.get("LOCAL_RANK", "0"))])
+        else:
+            dist.barrier()
 
 
 # --------------------------------------------------------------------------- CPU reference arm
