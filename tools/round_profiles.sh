@@ -1,6 +1,6 @@
 # Round measurement pass on the GPU box: tests, bench lines, ncu launch list + full captures.
 # Output: gpurun_out/r03_*  (copied into profiles/ afterwards)
-R=r03
+R=${R:-r04}
 O=gpurun_out
 python -c "import __graft_entry__ as g; g.smoke()" > $O/${R}_smoke.txt 2>&1
 timeout 900 python -m pytest tests -m gpu -q > $O/${R}_pytest_gpu.txt 2>&1
