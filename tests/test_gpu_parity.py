@@ -220,6 +220,12 @@ def test_overlapped_host_path_matches_eager_program(n):
     for nid in sb.leaf_solutions:
         np.testing.assert_array_equal(sa.leaf_solutions[nid], sb.leaf_solutions[nid])
         np.testing.assert_array_equal(sa.g_tab[nid], sb.g_tab[nid])
+    # result buffers: states that are kept alive are never overwritten by later solves
+    a.use_graphs = True
+    keep = [a.solve(f=f, g=lambda pts, s=s: s * g(pts)) for s in (1.0, 2.0, 3.0, 4.0)]
+    for s_, st in zip((1.0, 2.0, 3.0, 4.0), keep):
+        np.testing.assert_allclose(st.u, s_ * sa.u - (s_ - 1.0) * a.solve(f=f, g=lambda pts: 0 * g(pts)).u,
+                                   rtol=0, atol=1e-12 * np.abs(sa.u).max())
 
 
 class TestUnionDomains:
