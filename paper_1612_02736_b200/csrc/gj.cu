@@ -204,10 +204,20 @@ __global__ void gj_swapcopy_kernel(int n, int col_lo, int col_hi, int k0, int kb
   double* Wi = W.get(item);
 #pragma unroll 8
   for (int j = 0; j < kb; ++j) Wi[(long long)j * W.ld + c] = Mi[(long long)rowid[j] * ld + c];
+  // displaced rows (after the W reads of this column: a W source can be a move destination).
+  // Every move source is an original panel row and every destination lies outside the panel,
+  // so the loads of a group can all be issued before its stores (8 in flight instead of one
+  // dependent round trip per move)
   const int nm = moves[0];
-  for (int m = 0; m < nm; ++m) {
-    const int dst = moves[1 + 2 * m], src = moves[2 + 2 * m];
-    Mi[(long long)dst * ld + c] = Mi[(long long)src * ld + c];
+  const int m0 = 0, m1 = nm;
+  for (int mb = m0; mb < m1; mb += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (mb + u < m1) v[u] = Mi[(long long)moves[2 + 2 * (mb + u)] * ld + c];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (mb + u < m1) Mi[(long long)moves[1 + 2 * (mb + u)] * ld + c] = v[u];
   }
 }
 
@@ -322,9 +332,11 @@ static void swapcopy_range(int batch, int n, int col_lo, int col_hi, int k0, int
   if (nlog <= 0) return;
   for (int off = 0; off < batch; off += 65535) {
     const int bb = min(65535, batch - off);
-    dim3 g2((nlog + 127) / 128, bb);
-    gj_swapcopy_kernel<<<g2, 128, sizeof(int) * (n - k0 + 2 * kb + 4), s>>>(n, col_lo, col_hi, k0, kb, M, piv,
-                                                                            W, off);
+    // one thread per column; few matrices: 32-thread CTAs so the pass spreads over the SMs
+    const int nt = (long long)((nlog + 127) / 128) * bb >= 2 * sm_count() ? 128 : 32;
+    dim3 g2((nlog + nt - 1) / nt, bb);
+    gj_swapcopy_kernel<<<g2, nt, sizeof(int) * (n - k0 + 2 * kb + 4), s>>>(n, col_lo, col_hi, k0, kb, M, piv,
+                                                                           W, off);
   }
 }
 

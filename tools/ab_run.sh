@@ -1,8 +1,4 @@
-summ() { python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['ms_per_step'], d['roofline']['achieved'], d['solve_roofline']['frac'], d.get('timestep',{}).get('ms_per_step'))"; }
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -1 >> gpurun_out/ab.txt
-for v in "HPS_WIDE_MAXK=0" "HPS_WIDE_MAXK=256" "HPS_WIDE_MAXK=128"; do
-  echo "== cfg5 16rhs $v" >> gpurun_out/ab.txt
-  env $v timeout 300 python bench.py --config 5 --nrhs 16 --skip-cpu 2>&1 | summ >> gpurun_out/ab.txt 2>&1
-done
-python tools/sweep_steps.py --config 5 --nrhs 16 > gpurun_out/steps_cfg5_16.txt 2>&1
+timeout 600 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_parity.py -x -q 2>&1 | tail -1 >> gpurun_out/ab.txt
+for c in 5 3; do timeout 300 python tools/profile_build.py --config $c 2>&1 | grep -E "merge d[0-4] |leaf-build" >> gpurun_out/ab.txt; done
+python tools/build_reps.py 2>&1 | tail -7 >> gpurun_out/ab.txt
 cat gpurun_out/ab.txt
