@@ -214,6 +214,47 @@ def solve_fixtures():
     save("cfg5_n4.npz", **a)
 
 
+def fullsize_fixture():
+    """BASELINE configs 2-5 at their full sizes, run by the reference itself. The full solutions
+    are too large to commit, so the fixture keeps a fingerprint: norms of u, u on 2000 seeded
+    Gauss nodes, the complete tabulations of 24 seeded leaves, and (config 2) the error against
+    the manufactured solution."""
+    rng = np.random.default_rng(2024)
+
+    def fingerprint(tag, tree, spec, p, q, solve_kw=None, extra=None):
+        import time
+        t0 = time.perf_counter()
+        solver = build_stage(tree, spec, p, q)
+        st = solver.solve(**(solve_kw or {}))
+        ids = sorted(st.leaf_solutions)
+        pick = np.sort(rng.choice(len(ids), size=min(24, len(ids)), replace=False))
+        upick = np.sort(rng.choice(len(st.u), size=min(2000, len(st.u)), replace=False))
+        out = {"u_idx": upick, "u_vals": st.u[upick], "u_max": np.array([np.abs(st.u).max()]),
+               "u_l2": np.array([np.linalg.norm(st.u)]), "leaf_ids": np.array([ids[i] for i in pick]),
+               "leaf_sol": np.stack([st.leaf_solutions[ids[i]] for i in pick]),
+               "leaf_max": np.array([max(np.abs(v).max() for v in st.leaf_solutions.values())])}
+        if spec.u_exact is not None:
+            out["linf_error"] = np.array([linf_error(st, ReferenceSolution.analytic(spec.u_exact))])
+        out.update(extra or {})
+        save(f"full_{tag}.npz", **out)
+        print(tag, f"{time.perf_counter() - t0:.1f} s")
+
+    fingerprint("cfg2", build_uniform_tree(UNIT, 64), problems.config2_spec(), 16, 15)
+    fingerprint("cfg3", build_uniform_tree(UNIT, 32), problems.config3_spec(), 32, 31)
+    fingerprint("cfg4", build_balanced_refined_tree(8, (0.3, 0.7), 8, tree_factory=build_uniform_tree),
+                problems.config4_spec(), 16, 14)
+    # config 5: the first backward-Euler step of RHS 0 (g = u0[i_ci] / dt, f at t = dt)
+    dt = 1e-3
+    tree = build_uniform_tree(UNIT, 128)
+    u0 = problems.config5_initial(seed=0)
+    g = {}
+    for lf in tree.leaves():
+        geo = leaf_geometry(16, 15, lf.bounds.width, lf.bounds.height)
+        g[lf.id] = u0(stencil_for(lf.bounds, geo).cheb2d)[geo.stencil0.i_ci] / dt
+    fingerprint("cfg5", tree, problems.config5_spec(dt), 16, 15,
+                solve_kw={"f": lambda pts: problems.config5_dirichlet(pts, dt), "g": g})
+
+
 def cn_fixture():
     from specdtn.experiments import heat_problem
     from specdtn.timestepping import TimeStepConfig, cn_run
@@ -231,6 +272,9 @@ if __name__ == "__main__":
         raise SystemExit
     if "--only-plans" in _sys.argv:
         plan_fixture()
+        raise SystemExit
+    if "--only-full" in _sys.argv:
+        fullsize_fixture()
         raise SystemExit
     cn_fixture()
     spectral_fixture()

@@ -1,0 +1,60 @@
+"""BASELINE configs 2-5 at their FULL sizes on the GPU against fingerprints of the reference's own
+solution (tests/golden/make_golden.py --only-full: u on 2000 seeded Gauss nodes, 24 complete leaf
+tabulations, norms). Tolerances are the north star's: relative max-norm <= 1e-10 (<= 1e-9 at
+p = 32), relative to the maximum over the whole field; config 2's error against the manufactured
+solution must be within a factor of 2 of the reference's."""
+import numpy as np
+import pytest
+
+from hps_testutil import golden
+from oracle import hps_oracle as orc
+from paper_1612_02736_b200 import build_balanced_refined_tree, build_stage, build_uniform_tree, problems
+from paper_1612_02736_b200.reference import ReferenceSolution, linf_error
+
+pytestmark = pytest.mark.gpu
+UNIT = (0.0, 1.0, 0.0, 1.0)
+
+
+def _check(fx, st, tol):
+    u = np.asarray(st.u)
+    assert abs(np.abs(u).max() - fx["u_max"][0]) <= tol * fx["u_max"][0]
+    # | ||u|| - ||u_ref|| | <= ||u - u_ref||_2 <= sqrt(N) max|u - u_ref|
+    assert abs(np.linalg.norm(u) - fx["u_l2"][0]) <= tol * fx["u_max"][0] * np.sqrt(len(u))
+    assert np.abs(u[fx["u_idx"]] - fx["u_vals"]).max() <= tol * fx["u_max"][0]
+    sol = np.stack([st.leaf_solutions[int(i)] for i in fx["leaf_ids"]])
+    assert np.abs(sol - fx["leaf_sol"]).max() <= tol * fx["leaf_max"][0]
+
+
+def test_config2_full_size():
+    fx = golden("full_cfg2.npz")
+    spec = problems.config2_spec()
+    st = build_stage(build_uniform_tree(UNIT, 64), spec, 16, 15).solve()
+    _check(fx, st, 1e-10)
+    err = linf_error(st, ReferenceSolution.analytic(spec.u_exact))
+    ref_err = fx["linf_error"][0]
+    assert err <= 2.0 * ref_err, (err, ref_err)
+
+
+def test_config3_full_size():
+    fx = golden("full_cfg3.npz")
+    st = build_stage(build_uniform_tree(UNIT, 32), problems.config3_spec(), 32, 31).solve()
+    _check(fx, st, 1e-9)
+
+
+def test_config4_full_size():
+    fx = golden("full_cfg4.npz")
+    tree = build_balanced_refined_tree(8, (0.3, 0.7), 8)
+    assert len(tree.leaves()) == 175
+    st = build_stage(tree, problems.config4_spec(), 16, 14).solve()
+    _check(fx, st, 1e-10)
+
+
+def test_config5_full_size_first_step():
+    fx = golden("full_cfg5.npz")
+    dt = 1e-3
+    tree = build_uniform_tree(UNIT, 128)
+    solver = build_stage(tree, problems.config5_spec(dt), 16, 15)
+    u0 = problems.config5_initial(0)
+    tabs = {lf.id: u0(orc.leaf_points(lf.bounds, 16, 15)) for lf in tree.leaves()}
+    st = solver.solve(f=lambda pts: problems.config5_dirichlet(pts, dt), g=orc.be_loads(tabs, tree, 16, 15, dt))
+    _check(fx, st, 1e-10)
