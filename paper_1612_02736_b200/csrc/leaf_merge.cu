@@ -25,26 +25,37 @@ __global__ void __launch_bounds__(256) leaf_assemble_kernel(LeafAsmArgs a, int b
   double* dy = dx + p * p;
   double* dxx = dy + p * p;
   double* dyy = dxx + p * p;
+  double* cr = dyy + p * p;  // [ASM_ROWS][6] coefficient samples at this CTA's row points
+  int* ipos = reinterpret_cast<int*>(cr + 6 * ASM_ROWS);  // [P] position in i_ci, else -(1 + pos in i_ce)
+  const int leaf = blockIdx.y + batch_off;
+  const long long cstride = (long long)a.nleaf * P;
+  const double* cf = a.coef + (long long)leaf * P;
+  const int r0 = blockIdx.x * ASM_ROWS;
   for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
     dx[e] = a.dx[e];
     dy[e] = a.dy[e];
     dxx[e] = a.dxx[e];
     dyy[e] = a.dyy[e];
   }
+  for (int j = threadIdx.x; j < P; j += blockDim.x) {
+    const int ip = a.int_pos[j];
+    ipos[j] = ip >= 0 ? ip : -1 - a.ext_pos[j];
+  }
+  // all rows' coefficients staged up front: no dependent global loads inside the row loop
+  for (int e = threadIdx.x; e < ASM_ROWS * 6; e += blockDim.x) {
+    const int rr = e / 6, t = e - rr * 6, r = r0 + rr;
+    if (r < m) cr[e] = cf[t * cstride + (1 + r % pm) + p * (1 + r / pm)];
+  }
   __syncthreads();
-  const int leaf = blockIdx.y + batch_off;
-  const long long cstride = (long long)a.nleaf * P;
-  const double* cf = a.coef + (long long)leaf * P;
   double* aii = a.Aii.get(leaf);
   double* aie = a.Aie.get(leaf);
-  const int r0 = blockIdx.x * ASM_ROWS;
   for (int r = r0; r < min(m, r0 + ASM_ROWS); ++r) {
     const int i1 = 1 + r % pm, i2 = 1 + r / pm;
     const int k = i1 + p * i2;
-    const double c11 = cf[k], c12 = cf[cstride + k], c22 = cf[2 * cstride + k];
-    const double c1 = cf[3 * cstride + k], c2 = cf[4 * cstride + k], c0 = cf[5 * cstride + k];
-    for (int j = threadIdx.x; j < P; j += blockDim.x) {
-      const int j1 = j % p, j2 = j / p;
+    const double* c6 = cr + (r - r0) * 6;
+    const double c11 = c6[0], c12 = c6[1], c22 = c6[2], c1 = c6[3], c2 = c6[4], c0 = c6[5];
+    auto elem = [&](int j1, int j2) {
+      const int j = j1 + p * j2;
       const double d11 = (i2 == j2) ? dxx[i1 * p + j1] : 0.0;
       const double d12 = dy[i2 * p + j2] * dx[i1 * p + j1];
       const double d22 = (i1 == j1) ? dyy[i2 * p + j2] : 0.0;
@@ -56,18 +67,26 @@ __global__ void __launch_bounds__(256) leaf_assemble_kernel(LeafAsmArgs a, int b
       v += c1 * d1;
       v += c2 * d2;
       if (j == k) v += c0;
-      const int ip = a.int_pos[j];
+      const int ip = ipos[j];
       if (ip >= 0)
         aii[(long long)r * a.Aii.ld + ip] = v;
       else
-        aie[(long long)r * a.Aie.ld + a.ext_pos[j]] = v;
+        aie[(long long)r * a.Aie.ld + (-1 - ip)] = v;
+    };
+    if (p >= 32 && (int)blockDim.x % p == 0) {
+      // thread -> (j1, first j2) fixed for the CTA: no integer division per element (measured
+      // faster at p = 32, slower at p = 16)
+      const int j1 = (int)threadIdx.x % p, step = (int)blockDim.x / p;
+      for (int j2 = (int)threadIdx.x / p; j2 < p; j2 += step) elem(j1, j2);
+    } else {
+      for (int j = threadIdx.x; j < P; j += blockDim.x) elem(j % p, j / p);
     }
   }
 }
 
 int launch_leaf_assemble(const LeafAsmArgs& a, cudaStream_t s) {
   const int m = (a.p - 2) * (a.p - 2);
-  const size_t smem = sizeof(double) * 4 * a.p * a.p;
+  const size_t smem = sizeof(double) * (4 * a.p * a.p + 6 * ASM_ROWS) + sizeof(int) * a.p * a.p;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(leaf_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   for (int off = 0; off < a.nleaf; off += 65535) {
