@@ -361,7 +361,15 @@ int launch_gemm(const GemmArgs& g, int batch, int mode, cudaStream_t s) {
     // pipeline, 3 CTAs/SM (measured +3 % over 3 stages / 2 CTAs on the K = 64 GJ updates)
     const bool rmw = mode == MODE_GJ_UPD || g.beta != 0.0;
     if (mode == MODE_GEMM) {
-      if (rmw || g.N < 96) {
+      // 64-wide tiles also when they pad N much less than 128-wide ones (H = D F at p = 32:
+      // N = 900 -> 960 instead of 1024); HPS_GEMM_PAD64=0 disables
+      static int pad64 = -1;
+      if (pad64 < 0) {
+        const char* e = getenv("HPS_GEMM_PAD64");
+        pad64 = e ? atoi(e) : 1;
+      }
+      const bool narrow_pad = pad64 && 100 * ((g.N + 63) / 64 * 64) < 95 * ((g.N + 127) / 128 * 128);
+      if (rmw || g.N < 96 || narrow_pad) {
         if (gemm_variant() == 3) launch_big<MODE_GEMM, 64>(g, batch, s);
         else launch_big<MODE_GEMM, 64, 2>(g, batch, s);
       } else {

@@ -1,6 +1,8 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q 2>&1 | tail -1 >> gpurun_out/ab.txt
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:leaf_assemble --log-file gpurun_out/asm.csv python tools/ncu_target.py --config 3 --solves 0 > /dev/null 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:leaf_assemble --log-file gpurun_out/asm5.csv python tools/ncu_target.py --config 5 --solves 0 > /dev/null 2>&1
-python tools/launch_summary.py gpurun_out/asm.csv 1 >> gpurun_out/ab.txt; python tools/launch_summary.py gpurun_out/asm5.csv 1 >> gpurun_out/ab.txt
-for c in 3 5; do timeout 300 python tools/profile_build.py --config $c 2>&1 | grep -E "leaf-build" >> gpurun_out/ab.txt; done
+for v in "HPS_GEMM_PAD64=0" "HPS_GEMM_PAD64=1" "HPS_GEMM_PAD64=1 HPS_GEMM_VARIANT=3"; do
+echo "== $v" >> gpurun_out/ab.txt
+env $v timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:gemm_big --log-file gpurun_out/g.csv python tools/ncu_target.py --config 3 --solves 0 > /dev/null 2>&1
+python tools/launch_summary.py gpurun_out/g.csv 1 | grep "1024)" | head -4 >> gpurun_out/ab.txt
+env $v timeout 300 python tools/profile_build.py --config 3 2>&1 | grep -E "leaf-build" >> gpurun_out/ab.txt
+done
+timeout 600 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_parity.py -x -q 2>&1 | tail -1 >> gpurun_out/ab.txt
 cat gpurun_out/ab.txt
