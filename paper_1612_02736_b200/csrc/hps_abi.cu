@@ -65,9 +65,16 @@ int hps_gj_invert_batched(int batch, int n, int ncols, const hps_mat_batch* M, i
                    (cudaStream_t)stream, perm);
 }
 
+static long long colpart_bytes(int nleaf, int p) {
+  const long long m = (long long)(p - 2) * (p - 2);
+  if ((long long)p * p > 8 * 256) return 0;  // no fused |A_ii|_1 (leaf_merge.cu)
+  return align256(8LL * nleaf * ((m + leaf_assemble_rows() - 1) / leaf_assemble_rows()) * m);
+}
+
 long long hps_leaf_workspace_bytes(int nleaf, int p, int q) {
   const long long m = (long long)(p - 2) * (p - 2), b = 4LL * q, c = 4LL * (p - 1);
-  return align256(8 * nleaf * m * c) + align256(4 * nleaf * m) + hps_gj_workspace_bytes(nleaf, (int)m, (int)(m + b));
+  return align256(8 * nleaf * m * c) + align256(4 * nleaf * m) + colpart_bytes(nleaf, p) +
+         hps_gj_workspace_bytes(nleaf, (int)m, (int)(m + b));
 }
 
 int hps_leaf_build(const hps_leaf_batch* L, void* stream) {
@@ -78,7 +85,9 @@ int hps_leaf_build(const hps_leaf_batch* L, void* stream) {
   char* ws = (char*)L->workspace;
   double* aie = (double*)ws;
   int* piv = (int*)(ws + align256(8ull * nl * m * c));
-  void* gjw = ws + align256(8ull * nl * m * c) + align256(4ull * nl * m);
+  const long long cpb = colpart_bytes(nl, p);
+  double* colpart = cpb ? (double*)(ws + align256(8ull * nl * m * c) + align256(4ull * nl * m)) : nullptr;
+  void* gjw = ws + align256(8ull * nl * m * c) + align256(4ull * nl * m) + cpb;
   const long long sfs = (long long)m * (m + b);
 
   LeafAsmArgs a{};
@@ -93,6 +102,9 @@ int hps_leaf_build(const hps_leaf_batch* L, void* stream) {
   a.ext_pos = L->ext_pos;
   a.Aii = dense(L->fs, sfs, m + b);
   a.Aie = dense(aie, (long long)m * c, c);
+  // |A_ii|_1 (the rcond rule, leaf.py:113-115) from the assembly itself: no separate pass over A_ii
+  a.colpart = L->anorm ? colpart : nullptr;
+  a.anorm = L->anorm;
   int rc = launch_leaf_assemble(a, s);
   if (rc) return rc;
 
@@ -109,8 +121,8 @@ int hps_leaf_build(const hps_leaf_batch* L, void* stream) {
   if ((rc = launch_gemm(g, nl, MODE_GEMM, s))) return rc;
 
   // [F | S] = inv(A_ii) [I | -A_ie L]
-  if ((rc = gj_invert(nl, m, m + b, dense(L->fs, sfs, m + b), piv, (double*)gjw, L->anorm, L->ainvnorm,
-                      L->status, s, L->perm)))
+  if ((rc = gj_invert(nl, m, m + b, dense(L->fs, sfs, m + b), piv, (double*)gjw, colpart ? nullptr : L->anorm,
+                      L->ainvnorm, L->status, s, L->perm)))
     return rc;
 
   // H = D_fi F   (leaf.py:162; exterior rows of F are zero)

@@ -62,7 +62,10 @@ struct LeafAsmArgs {
   const int* ext_pos;      // [p*p] position in i_ce or -1
   MatB Aii;                // m x (m+b) (only the first m columns written)
   MatB Aie;                // m x c
+  double* colpart;         // nullable: [nleaf][row blocks][m] partial column sums of |A_ii|
+  double* anorm;           // with colpart: |A_ii|_1 per leaf (leaf_assemble_rows() rows per block)
 };
+int leaf_assemble_rows();
 int launch_leaf_assemble(const LeafAsmArgs& a, cudaStream_t s);
 
 // Merge gather: builds [Delta | -Ta31 | Tb32], Tei = [Ta13; Tb23], Tnew = blkdiag(Ta11, Tb22)

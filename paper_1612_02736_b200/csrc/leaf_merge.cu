@@ -49,6 +49,12 @@ __global__ void __launch_bounds__(256) leaf_assemble_kernel(LeafAsmArgs a, int b
   __syncthreads();
   double* aii = a.Aii.get(leaf);
   double* aie = a.Aie.get(leaf);
+  // |A_ii|_1 on the fly: each thread keeps the |.| sums of its own columns over this CTA's rows
+  // (columns of a thread: j = threadIdx.x + t*blockDim.x, t < ASM_COLS)
+  constexpr int ASM_COLS = 8;
+  double csum[ASM_COLS];
+#pragma unroll
+  for (int t = 0; t < ASM_COLS; ++t) csum[t] = 0.0;
   for (int r = r0; r < min(m, r0 + ASM_ROWS); ++r) {
     const int i1 = 1 + r % pm, i2 = 1 + r / pm;
     const int k = i1 + p * i2;
@@ -72,15 +78,59 @@ __global__ void __launch_bounds__(256) leaf_assemble_kernel(LeafAsmArgs a, int b
         aii[(long long)r * a.Aii.ld + ip] = v;
       else
         aie[(long long)r * a.Aie.ld + (-1 - ip)] = v;
+      return ip >= 0 ? fabs(v) : 0.0;
     };
+    // (both mappings visit j = threadIdx.x + t*blockDim.x, so csum[t] is always column j's sum)
     if (p >= 32 && (int)blockDim.x % p == 0) {
       // thread -> (j1, first j2) fixed for the CTA: no integer division per element (measured
       // faster at p = 32, slower at p = 16)
       const int j1 = (int)threadIdx.x % p, step = (int)blockDim.x / p;
-      for (int j2 = (int)threadIdx.x / p; j2 < p; j2 += step) elem(j1, j2);
+      int t = 0;
+      for (int j2 = (int)threadIdx.x / p; j2 < p; j2 += step, ++t) {
+        const double av = elem(j1, j2);
+        if (t < ASM_COLS) csum[t] += av;
+      }
     } else {
-      for (int j = threadIdx.x; j < P; j += blockDim.x) elem(j % p, j / p);
+      int t = 0;
+      for (int j = threadIdx.x; j < P; j += blockDim.x, ++t) {
+        const double av = elem(j % p, j / p);
+        if (t < ASM_COLS) csum[t] += av;
+      }
     }
+  }
+  if (a.colpart) {
+    double* cp = a.colpart + ((long long)leaf * gridDim.x + blockIdx.x) * m;
+    int t = 0;
+    for (int j = threadIdx.x; j < P && t < ASM_COLS; j += blockDim.x, ++t)
+      if (ipos[j] >= 0) cp[ipos[j]] = csum[t];
+  }
+}
+
+int leaf_assemble_rows() { return ASM_ROWS; }
+
+// |A_ii|_1 per leaf from the assembly's partial column sums (row blocks summed in order)
+__global__ void __launch_bounds__(256) colpart_norm_kernel(int m, int nrb, const double* colpart, double* anorm,
+                                                           int batch_off) {
+  const int leaf = blockIdx.x + batch_off;
+  const double* cp = colpart + (long long)leaf * nrb * m;
+  double best = 0.0;
+  for (int c = threadIdx.x; c < m; c += blockDim.x) {
+    double sum = 0.0;
+    for (int rb = 0; rb < nrb; ++rb) sum += cp[(long long)rb * m + c];
+    best = (sum > best || sum != sum) ? sum : best;
+  }
+  __shared__ double red[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double t = __shfl_xor_sync(0xffffffffu, best, o);
+    best = (t > best || t != t) ? t : best;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = (red[w] > v || red[w] != red[w]) ? red[w] : v;
+    anorm[leaf] = v;
   }
 }
 
@@ -89,10 +139,16 @@ int launch_leaf_assemble(const LeafAsmArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(double) * (4 * a.p * a.p + 6 * ASM_ROWS) + sizeof(int) * a.p * a.p;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(leaf_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // colpart needs every column of a thread in csum[]: P <= 8 * 256 (p <= 45)
+  if (a.colpart && a.p * a.p > 8 * 256) return 1;
+  const int nrb = (m + ASM_ROWS - 1) / ASM_ROWS;
   for (int off = 0; off < a.nleaf; off += 65535) {
-    dim3 grid((m + ASM_ROWS - 1) / ASM_ROWS, min(65535, a.nleaf - off));
+    dim3 grid(nrb, min(65535, a.nleaf - off));
     leaf_assemble_kernel<<<grid, 256, smem, s>>>(a, off);
   }
+  if (a.colpart && a.anorm)
+    for (int off = 0; off < a.nleaf; off += 65535)
+      colpart_norm_kernel<<<min(65535, a.nleaf - off), 256, 0, s>>>(m, nrb, a.colpart, a.anorm, off);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 

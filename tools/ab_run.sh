@@ -1,6 +1,4 @@
-summ() { python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['ms_per_step'], d['solve_roofline']['frac'])"; }
-for v in "HPS_PDL=1" "HPS_PDL=0"; do
-  echo "== cfg2 $v" >> gpurun_out/ab.txt
-  env $v timeout 300 python bench.py --config 2 --skip-cpu --steps 200 2>&1 | summ >> gpurun_out/ab.txt 2>&1
-done
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -1 >> gpurun_out/ab.txt
+for c in 3 5 2; do timeout 300 python tools/profile_build.py --config $c 2>&1 | grep -E "leaf-build" >> gpurun_out/ab.txt; done
+python tools/build_reps.py 2>&1 | grep -E "^(5|2) 4" >> gpurun_out/ab.txt
 cat gpurun_out/ab.txt
