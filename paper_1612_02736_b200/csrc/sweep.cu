@@ -328,6 +328,136 @@ __global__ void __launch_bounds__(256, 4) gemv_dmma_kernel(GemvArgs a, int rpc, 
   }
 }
 
+// Multi-RHS (3..16) steps of small items (deep tree levels: thousands of items of 15..360 rows
+// and K <= ~300): IPC items per CTA, each owned by a group of 8/IPC warps. A group stages its
+// item's whole x (K x NRP, padded stride) in shared memory, then each warp takes 16-row groups
+// of the item and runs the k4 steps on DMMA tiles with A fragments straight from global memory.
+// No k-split, no cross-warp reduction. The one-item-per-CTA kernel above left the 8192-item
+// levels of config 5 at 0.4-0.9 TB/s. mode2 = 3 (w3 = X d as a partial sum over [0, K2)) is
+// two passes over the column ranges.
+template <int NRP, int IPC>
+__global__ void __launch_bounds__(256) gemv_dmma_multi_kernel(GemvArgs a) {
+  extern __shared__ double xsm[];
+  constexpr int XLD = NRP + 4;
+  constexpr int NT = NRP / 8;
+  constexpr int GW = 8 / IPC;  // warps per item
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = warp / GW, gw = warp % GW;
+  const int item = blockIdx.x * IPC + grp;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int R = a.R, K = a.K, nrhs = a.nrhs;
+  const int kp = (K + 3) & ~3;
+  double* xs = xsm + (size_t)grp * kp * XLD;
+  pdl_trigger();
+  pdl_wait();
+  if (item >= a.nitems) return;  // whole group
+  const int* xi = a.xidx + (long long)item * a.xstride;
+  const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
+  gather_x<NRP, 4>(xs, XLD, xi, x2, a.pool, nrhs, K, kp, (int)threadIdx.x - grp * GW * 32, GW * 32);
+  if (GW == 1)
+    __syncwarp();
+  else
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(GW * 32) : "memory");
+  const double* Ai = a.A.get(item);
+  const long long lda = a.A.ld;
+  const int* ai = a.aidx ? a.aidx + (long long)item * a.ostride : nullptr;
+  const int* oi = a.oidx + (long long)item * a.ostride;
+  const int* o2 = a.mode2 == 3 ? a.o2idx + (long long)item * a.ostride : nullptr;
+  const int ksplit = a.mode2 == 3 ? a.K2 : 0;
+  double* pool = a.pool;
+  for (int rbase = gw * 16; rbase < R; rbase += GW * 16) {
+    const int ra = rbase + gq, rb = rbase + 8 + gq;
+    const bool la = ra < R, lb = rb < R;
+    const double* rowa = Ai + (long long)(la ? ra : 0) * lda;
+    const double* rowb = Ai + (long long)(lb ? rb : 0) * lda;
+    double acc[2][NT][2], accw[2][NT][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int n = 0; n < NT; ++n) acc[i][n][0] = acc[i][n][1] = accw[i][n][0] = accw[i][n][1] = 0.0;
+    // pass 0: columns [0, ksplit) into accw (mode2 = 3 only); pass 1: [ksplit, K) into acc
+    for (int pass = ksplit > 0 ? 0 : 1; pass < 2; ++pass) {
+      const int klo = pass ? ksplit : 0, khi = pass ? K : ksplit;
+      for (int k = klo & ~3; k < khi; k += 16) {
+        double va[4], vb[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int kk = k + 4 * u + tq;
+          const bool kin = kk >= klo && kk < khi;
+          va[u] = (kin && la) ? __ldg(rowa + kk) : 0.0;
+          vb[u] = (kin && lb) ? __ldg(rowb + kk) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int kb = k + 4 * u;
+          if (kb >= khi) break;
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            const double bv = xs[(kb + tq) * XLD + n * 8 + gq];
+            if (pass) {
+              dmma8x8x4(acc[0][n][0], acc[0][n][1], va[u], bv);
+              dmma8x8x4(acc[1][n][0], acc[1][n][1], vb[u], bv);
+            } else {
+              dmma8x8x4(accw[0][n][0], accw[0][n][1], va[u], bv);
+              dmma8x8x4(accw[1][n][0], accw[1][n][1], vb[u], bv);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int r = i ? rb : ra;
+      if (r >= R) continue;
+#pragma unroll
+      for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = n * 8 + tq * 2 + h;
+          if (j >= nrhs) continue;
+          double v = acc[i][n][h] + accw[i][n][h];
+          if (o2) pool[(long long)o2[r] * nrhs + j] = accw[i][n][h];
+          if (ai) v += pool[(long long)ai[r] * nrhs + j];
+          pool[(long long)oi[r] * nrhs + j] = v;
+        }
+    }
+  }
+}
+
+template <int NRP>
+static bool launch_dmma_multi(const GemvArgs& a, cudaStream_t s) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("HPS_DMMA_MULTI");
+    on = e ? atoi(e) : 1;
+  }
+  // measured (config 5, 16 RHS): faster than the one-item-per-CTA kernel only for the split-output
+  // downward steps of the deepest levels (R <= 32: one launch instead of two; 8192 items 232 ->
+  // 123 us); slower for the upward steps, whose rows the 8 warps of a CTA split better
+  if (!on || a.mode2 != 3 || a.aidx || a.R > 32) return false;
+  const size_t per_item = sizeof(double) * (size_t)((a.K + 3) & ~3) * (NRP + 4);
+  int ipc = 1;
+  while (ipc < 8 && (long long)a.nitems / (2 * ipc) >= 2 * 148 && per_item * 2 * ipc <= 96 * 1024) ipc *= 2;
+  if (ipc == 1 || a.R > 16 * 8 * 4) return false;  // one item per CTA: the kernel above
+  const size_t smem = per_item * ipc;
+  const dim3 grid((unsigned)((a.nitems + ipc - 1) / ipc));
+  switch (ipc) {
+    case 2:
+      cudaFuncSetAttribute(gemv_dmma_multi_kernel<NRP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      launch_k(gemv_dmma_multi_kernel<NRP, 2>, grid, dim3(256), smem, s, a);
+      break;
+    case 4:
+      cudaFuncSetAttribute(gemv_dmma_multi_kernel<NRP, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      launch_k(gemv_dmma_multi_kernel<NRP, 4>, grid, dim3(256), smem, s, a);
+      break;
+    default:
+      cudaFuncSetAttribute(gemv_dmma_multi_kernel<NRP, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      launch_k(gemv_dmma_multi_kernel<NRP, 8>, grid, dim3(256), smem, s, a);
+      break;
+  }
+  return true;
+}
+
 // Staged-x sweep kernel for nrhs <= 2 with an optional fused second stage (tail / chain).
 // Rows are processed by groups of L lanes (L = 4..32 chosen from K so short rows do not idle
 // lanes), 8 independent loads in flight per lane, group-wide shuffle reduction.
@@ -744,6 +874,10 @@ int launch_gemv_gather(const GemvArgs& a, cudaStream_t s) {
     if (ok) return cudaGetLastError() == cudaSuccess ? 0 : 2;
   }
   if (a.nrhs > 2 && launch_gemv_tma(a, s)) return cudaGetLastError() == cudaSuccess ? 0 : 2;
+  if (a.nrhs > 2 && a.nrhs <= 16 && a.R > 1 && !a.A.ptrs) {
+    const bool ok = a.nrhs <= 8 ? launch_dmma_multi<8>(a, s) : launch_dmma_multi<16>(a, s);
+    if (ok) return cudaGetLastError() == cudaSuccess ? 0 : 2;
+  }
   if (a.mode2 == 3 && a.nrhs > 2) {
     // split output on the multi-RHS path: w = A[:, :K2] x[:K2] -> o2idx, then
     // y = A[:, K2:] x[K2:] + w -> oidx (the same operator bytes, two launches)
