@@ -37,7 +37,7 @@ __device__ long long gc_prof[8];
 #define GC_T(i)
 #endif
 
-constexpr int GC_CL = 8;         // CTAs per cluster (portable size)
+// CTAs per cluster: 8 (portable) or 16 (non-portable, opt-in; HPS_GJ_CL=16)
 constexpr int GC_THREADS = 256;
 constexpr int GC_NBMAX = 64;
 constexpr int GC_SB = 8;         // sub-block width
@@ -51,28 +51,30 @@ struct GcArgs {
 };
 
 // shared-memory layout (doubles) shared by the kernel and gj_cluster_smem
+template <int CL>
 struct GcLayout {
   int rl, nb, ldb;
   __host__ __device__ GcLayout(int rl_, int nb_) : rl(rl_), nb(nb_), ldb(nb_ + 1) {}
   static constexpr int BOX = 2 + GC_NBMAX;                           // best, row id, candidate row
   __host__ __device__ size_t b() const { return 0; }                   // rl x ldb own rows
   __host__ __device__ size_t box() const { return (size_t)rl * ldb; }  // [2][CL][BOX] inbox
-  __host__ __device__ size_t cjrow() const { return box() + 2 * GC_CL * BOX; }  // [2][NBMAX]
+  __host__ __device__ size_t cjrow() const { return box() + 2 * CL * BOX; }  // [2][NBMAX]
   __host__ __device__ size_t cp() const { return cjrow() + 2 * GC_NBMAX; }      // [SB][NBMAX+1]
   __host__ __device__ size_t red() const { return cp() + GC_SB * (GC_NBMAX + 1); }  // [warps][2]
   __host__ __device__ size_t ints() const { return red() + 2 * (GC_THREADS / 32); }  // spiv[nb]
   __host__ __device__ size_t total() const { return ints() + GC_NBMAX / 2 + 1; }
 };
 
-__global__ void __cluster_dims__(GC_CL, 1, 1) __launch_bounds__(GC_THREADS, 1) gj_cluster_kernel(GcArgs a) {
+template <int CL>
+__global__ void __launch_bounds__(GC_THREADS, 1) gj_cluster_kernel(GcArgs a) {
   extern __shared__ double sm[];
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
-  const int item = blockIdx.x / GC_CL;
+  const int item = blockIdx.x / CL;
   const int n = a.n, nb = a.nb, k0 = a.k0, rl = a.rl;
-  const GcLayout L(rl, nb);
+  const GcLayout<CL> L(rl, nb);
   const int ldb = L.ldb;
-  constexpr int BOX = GcLayout::BOX;
+  constexpr int BOX = GcLayout<CL>::BOX;
   constexpr int CPLD = GC_NBMAX + 1;
   double* B = sm + L.b();
   double* box = sm + L.box();
@@ -85,8 +87,11 @@ __global__ void __cluster_dims__(GC_CL, 1, 1) __launch_bounds__(GC_THREADS, 1) g
   const long long ld = a.M.ld;
   const int r0 = rank * rl;
   // warp w pushes this CTA's candidate (and row cj when owned) into CTA w's inbox
+  // (CL = 16: warp w also serves CTA w + 8)
   double* peer_box = cluster.map_shared_rank(box, warp);
   double* peer_cj = cluster.map_shared_rank(cjrow, warp);
+  double* peer_box2 = CL > 8 ? cluster.map_shared_rank(box, warp + 8) : nullptr;
+  double* peer_cj2 = CL > 8 ? cluster.map_shared_rank(cjrow, warp + 8) : nullptr;
 
   for (int e = tid; e < rl * nb; e += GC_THREADS) {
     const int r = e / nb, c = e - r * nb;
@@ -136,29 +141,32 @@ __global__ void __cluster_dims__(GC_CL, 1, 1) __launch_bounds__(GC_THREADS, 1) g
         if (vw > b || (vw == b && iw < bix)) { b = vw; bix = iw; }
       }
       // 2. push: warp w writes {best, row, candidate row} into CTA w's inbox slot [par][rank]
-      double* dst = peer_box + ((size_t)par * GC_CL + rank) * BOX;
-      if (lane == 0) {
-        dst[0] = b;
-        dst[1] = (double)bix;
+#pragma unroll
+      for (int h = 0; h < (CL > 8 ? 2 : 1); ++h) {
+        double* dst = (h ? peer_box2 : peer_box) + ((size_t)par * CL + rank) * BOX;
+        if (lane == 0) {
+          dst[0] = b;
+          dst[1] = (double)bix;
+        }
+        if (bix < n)
+          for (int c = lane; c < nb; c += 32) dst[2 + c] = B[(bix - r0) * ldb + c];
+        if (cj >= r0 && cj < r0 + rl)
+          for (int c = lane; c < nb; c += 32) (h ? peer_cj2 : peer_cj)[par * GC_NBMAX + c] = B[(cj - r0) * ldb + c];
       }
-      if (bix < n)
-        for (int c = lane; c < nb; c += 32) dst[2 + c] = B[(bix - r0) * ldb + c];
-      if (cj >= r0 && cj < r0 + rl)
-        for (int c = lane; c < nb; c += 32) peer_cj[par * GC_NBMAX + c] = B[(cj - r0) * ldb + c];
     }
     GC_T(0);
     cluster.sync();  // the only cluster barrier per column (release / acquire of the pushes)
     GC_T(1);
     // 3. winner from the local inbox (every warp: lane c < CL reads candidate c, shuffle reduce)
-    const double* mybox = box + (size_t)par * GC_CL * BOX;
+    const double* mybox = box + (size_t)par * CL * BOX;
     double vb = -2.0;
     int pr = n, owner = lane;
-    if (lane < GC_CL) {
+    if (lane < CL) {
       vb = mybox[lane * BOX];
       pr = (int)mybox[lane * BOX + 1];
     }
 #pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
+    for (int o = CL / 2; o > 0; o >>= 1) {
       const double ov = __shfl_xor_sync(0xffffffffu, vb, o);
       const int oi = __shfl_xor_sync(0xffffffffu, pr, o);
       const int oo = __shfl_xor_sync(0xffffffffu, owner, o);
@@ -279,9 +287,19 @@ __global__ void __cluster_dims__(GC_CL, 1, 1) __launch_bounds__(GC_THREADS, 1) g
   if (tid == 0 && rank == 0 && flag && a.status) a.status[item] |= 1;
 }
 
+static int gc_cl() {
+  static int cl = -1;  // HPS_GJ_CL: CTAs per cluster, 8 (portable) or 16 (non-portable)
+  if (cl < 0) {
+    const char* e = getenv("HPS_GJ_CL");
+    cl = (e && atoi(e) == 16) ? 16 : 8;
+  }
+  return cl;
+}
+
 size_t gj_cluster_smem(int n, int nb) {
-  const int rl = (n + GC_CL - 1) / GC_CL;
-  return sizeof(double) * GcLayout(rl, nb).total();
+  const int cl = gc_cl();
+  const int rl = (n + cl - 1) / cl;
+  return sizeof(double) * (cl == 16 ? GcLayout<16>(rl, nb).total() : GcLayout<8>(rl, nb).total());
 }
 
 // measured faster than the three-level fused path only for n >= ~900 (root and level-1 merges)
@@ -294,8 +312,32 @@ bool gj_cluster_ok(int n, int nb) {
   return n >= nmin && nb <= GC_NBMAX && gj_cluster_smem(n, nb) <= 200 * 1024;
 }
 
+template <int CL>
+static int launch_cl(const GcArgs& a, size_t smem, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(gj_cluster_kernel<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (CL > 8) cudaFuncSetAttribute(gj_cluster_kernel<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.batch * CL);
+  cfg.blockDim = dim3(GC_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gj_cluster_kernel<CL>, a) == cudaSuccess ? 0 : 2;
+}
+
 int launch_gj_cluster(int batch, int n, int k0, int nb, MatB M, int* piv, int* status, cudaStream_t s) {
   if (!gj_cluster_ok(n, nb)) return 1;
+  const int cl = gc_cl();
   GcArgs a{};
   a.batch = batch;
   a.n = n;
@@ -304,15 +346,9 @@ int launch_gj_cluster(int batch, int n, int k0, int nb, MatB M, int* piv, int* s
   a.M = M;
   a.piv = piv;
   a.status = status;
-  a.rl = (n + GC_CL - 1) / GC_CL;
+  a.rl = (n + cl - 1) / cl;
   const size_t smem = gj_cluster_smem(n, nb);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(gj_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
-  gj_cluster_kernel<<<batch * GC_CL, GC_THREADS, smem, s>>>(a);
-  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+  return cl == 16 ? launch_cl<16>(a, smem, s) : launch_cl<8>(a, smem, s);
 }
 
 }  // namespace hps
