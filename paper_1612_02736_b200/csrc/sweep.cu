@@ -590,6 +590,9 @@ __device__ __forceinline__ void rows_dot(const double* __restrict__ A, long long
 
 __host__ __device__ inline int lanes_for(int K) { return K <= 16 ? 4 : (K <= 48 ? 8 : (K <= 128 ? 16 : 32)); }
 
+static __device__ __constant__ int c_pre_index = 1;
+__device__ __forceinline__ bool pre_index() { return c_pre_index != 0; }
+
 // One work unit of a sweep step: item `item`, row chunk `chunk` of `nchunks` (rows_per_cta rows).
 template <int NR, bool VEC, int RB = 2, int U = 4, bool PDL = false>
 __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chunk, int nchunks, int rows_per_cta,
@@ -611,8 +614,32 @@ __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chun
     const uintptr_t hi = (reinterpret_cast<uintptr_t>(rp + K) + 15) & ~(uintptr_t)15;
     prefetch_l2_bulk(reinterpret_cast<const void*>(lo), (unsigned)(hi - lo));
   }
-  if (PDL) pdl_wait();
-  gather_x<NR>(xs, NR, xi, x2, pool, nrhs, K, K);
+  if (NR == 1 && PDL && K <= 2 * (int)blockDim.x && pre_index()) {
+    // single RHS, short x: the gather indices are static, so they are loaded before the
+    // programmatic-launch wait; after it only the pool rows remain on the critical path
+    int i1[2], i2[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int k = threadIdx.x + u * blockDim.x;
+      i1[u] = k < K ? __ldg(xi + k) : -1;
+      i2[u] = (k < K && x2) ? __ldg(x2 + k) : -1;
+    }
+    pdl_wait();
+    double v[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      v[u] = i1[u] >= 0 ? pool[i1[u]] : 0.0;
+      if (i2[u] >= 0) v[u] -= pool[i2[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int k = threadIdx.x + u * blockDim.x;
+      if (k < K) xs[k] = v[u];
+    }
+  } else {
+    if (PDL) pdl_wait();
+    gather_x<NR>(xs, NR, xi, x2, pool, nrhs, K, K);
+  }
   __syncthreads();
   rows_dot<NR, VEC, RB, U>(Ai, a.A.ld, a.R, r0, r1, K, lanes_for(K), xs,
                            a.aidx ? a.aidx + (long long)item * a.ostride : nullptr,
@@ -754,6 +781,15 @@ static int variant_of_env() {
 
 template <int NR>
 static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
+  {
+    static bool pre_set = false;  // HPS_PRE_INDEX=0: gather indices after the launch wait
+    if (!pre_set) {
+      const char* e = getenv("HPS_PRE_INDEX");
+      const int v = (e && atoi(e) == 0) ? 0 : 1;
+      cudaMemcpyToSymbol(c_pre_index, &v, sizeof(int));
+      pre_set = true;
+    }
+  }
   {
     static int old = -1;
     if (old < 0) {
