@@ -17,6 +17,11 @@ namespace hps {
 
 constexpr int SW_THREADS = 256;
 
+// 1: single-RHS kernels load their (static) gather indices before the programmatic-launch wait
+// (bit mask: 1 staged-x row kernel, 2 gather kernel, 4 multi-item kernel, 8 one-row kernel)
+static __device__ __constant__ int c_pre_index = 15;
+__device__ __forceinline__ bool pre_index(int bit = 1) { return (c_pre_index & bit) != 0; }
+
 // every sweep launch carries the programmatic-serialization attribute (HPS_PDL=0 disables)
 static bool pdl_enabled() {
   static int on = -1;
@@ -107,7 +112,27 @@ __global__ void __launch_bounds__(SW_THREADS) gemv_gather_kernel(GemvArgs a, int
     const uintptr_t hi = (reinterpret_cast<uintptr_t>(rp + K) + 15) & ~(uintptr_t)15;
     prefetch_l2_bulk(reinterpret_cast<const void*>(lo), (unsigned)(hi - lo));
   }
-  pdl_wait();
+  // single RHS, one chunk: the static gather indices are loaded before the launch wait
+  const bool pre = NR == 1 && a.mode2 == 0 && K <= kchunk && K <= 2 * SW_THREADS && pre_index(2);
+  if (pre) {
+    int i1[2], i2[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int k = tid + u * SW_THREADS;
+      i1[u] = k < K ? __ldg(xi + k) : -1;
+      i2[u] = (k < K && x2) ? __ldg(x2 + k) : -1;
+    }
+    pdl_wait();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int k = tid + u * SW_THREADS;
+      double v = i1[u] >= 0 ? pool[i1[u]] : 0.0;
+      if (i2[u] >= 0) v -= pool[i2[u]];
+      if (k < K) xs[k] = v;
+    }
+  } else {
+    pdl_wait();
+  }
 
   // mode2 = 3: chunk boundaries align with K2 and the partial sum over columns [0, K2) is also
   // stored at o2idx (parent down: u3 = [X | S][d; u_ext] writes w3 = X d on the way)
@@ -123,7 +148,7 @@ __global__ void __launch_bounds__(SW_THREADS) gemv_gather_kernel(GemvArgs a, int
       }
     }
     __syncthreads();
-    for (int e = tid; e < kc * NR; e += SW_THREADS) {
+    for (int e = pre ? kc * NR : tid; e < kc * NR; e += SW_THREADS) {  // pre: x already staged
       const int k = e / NR, j = e - k * NR;
       double v = 0.0;
       if (j < nrhs) {
@@ -590,9 +615,6 @@ __device__ __forceinline__ void rows_dot(const double* __restrict__ A, long long
 
 __host__ __device__ inline int lanes_for(int K) { return K <= 16 ? 4 : (K <= 48 ? 8 : (K <= 128 ? 16 : 32)); }
 
-static __device__ __constant__ int c_pre_index = 1;
-__device__ __forceinline__ bool pre_index() { return c_pre_index != 0; }
-
 // One work unit of a sweep step: item `item`, row chunk `chunk` of `nchunks` (rows_per_cta rows).
 template <int NR, bool VEC, int RB = 2, int U = 4, bool PDL = false>
 __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chunk, int nchunks, int rows_per_cta,
@@ -691,11 +713,31 @@ __global__ void __launch_bounds__(256) sweep_multi_kernel(GemvArgs a, int batch_
       prefetch_l2_bulk(reinterpret_cast<const void*>(lo), (unsigned)(hi - lo));
     }
   }
-  pdl_wait();
-  if (!live) return;  // the whole group shares the item
-  const int* xi = a.xidx + (long long)item * a.xstride;
-  const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
-  gather_x<NR>(xs, NR, xi, x2, a.pool, nrhs, K, K, gtid, GT);
+  const int* xi = live ? a.xidx + (long long)item * a.xstride : nullptr;
+  const int* x2 = (live && a.x2idx) ? a.x2idx + (long long)item * a.xstride : nullptr;
+  if (NR == 1 && K <= 2 * GT && pre_index(4)) {
+    // single RHS: the static gather indices are loaded before the launch wait
+    int i1[2], i2[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int k = gtid + u * GT;
+      i1[u] = (live && k < K) ? __ldg(xi + k) : -1;
+      i2[u] = (k < K && x2) ? __ldg(x2 + k) : -1;
+    }
+    pdl_wait();
+    if (!live) return;  // the whole group shares the item
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int k = gtid + u * GT;
+      double v = i1[u] >= 0 ? a.pool[i1[u]] : 0.0;
+      if (i2[u] >= 0) v -= a.pool[i2[u]];
+      if (k < K) xs[k] = v;
+    }
+  } else {
+    pdl_wait();
+    if (!live) return;  // the whole group shares the item
+    gather_x<NR>(xs, NR, xi, x2, a.pool, nrhs, K, K, gtid, GT);
+  }
   if (GT == 32)
     __syncwarp();
   else
@@ -785,7 +827,7 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
     static bool pre_set = false;  // HPS_PRE_INDEX=0: gather indices after the launch wait
     if (!pre_set) {
       const char* e = getenv("HPS_PRE_INDEX");
-      const int v = (e && atoi(e) == 0) ? 0 : 1;
+      const int v = e ? atoi(e) : 15;
       cudaMemcpyToSymbol(c_pre_index, &v, sizeof(int));
       pre_set = true;
     }
@@ -880,15 +922,39 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
 // (item, rhs), so thousands of tiny items do not each occupy a CTA.
 __global__ void __launch_bounds__(256) gemv_row1_kernel(GemvArgs a) {
   pdl_trigger();
-  pdl_wait();
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (long long)a.nitems * a.nrhs) return;
-  const int item = (int)(e / a.nrhs), j = (int)(e - (long long)item * a.nrhs);
-  const double* A = a.A.get(item);
+  const bool live = e < (long long)a.nitems * a.nrhs;
+  const int item = live ? (int)(e / a.nrhs) : 0, j = live ? (int)(e - (long long)item * a.nrhs) : 0;
   const int* xi = a.xidx + (long long)item * a.xstride;
   const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
+  // the indices (static) before the launch wait, the pool values after it
+  constexpr int KP = 8;
+  const bool pre = pre_index(8);
+  int i1[KP], i2[KP];
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    i1[k] = (pre && live && k < a.K) ? __ldg(xi + k) : -1;
+    i2[k] = (pre && live && k < a.K && x2) ? __ldg(x2 + k) : -1;
+  }
+  pdl_wait();
+  if (!pre && live) {
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      i1[k] = k < a.K ? xi[k] : -1;
+      i2[k] = (k < a.K && x2) ? x2[k] : -1;
+    }
+  }
+  if (!live) return;
+  const double* A = a.A.get(item);
   double acc = 0.0;
-  for (int k = 0; k < a.K; ++k) {
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    if (k >= a.K) break;
+    double v = a.pool[(long long)i1[k] * a.nrhs + j];
+    if (i2[k] >= 0) v -= a.pool[(long long)i2[k] * a.nrhs + j];
+    acc = fma(A[k], v, acc);
+  }
+  for (int k = KP; k < a.K; ++k) {
     double v = a.pool[(long long)xi[k] * a.nrhs + j];
     if (x2 && x2[k] >= 0) v -= a.pool[(long long)x2[k] * a.nrhs + j];
     acc = fma(A[k], v, acc);
