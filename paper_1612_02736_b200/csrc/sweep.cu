@@ -51,7 +51,7 @@ static void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
 // j < nrhs; zero for kc <= k < kp or j >= nrhs. GU elements per thread are issued together so
 // the index -> value load chains overlap: one memory round trip per GU elements, not per element
 // (the per-element loop left the multi-RHS leaf steps stalled on the gather, r01 ncu).
-template <int NRP, int GU = 8>
+template <int NRP, int GU = 8, bool PLAIN = false>
 __device__ __forceinline__ void gather_x(double* dst, int ld, const int* __restrict__ xi,
                                          const int* __restrict__ x2, const double* pool, int nrhs, int kc,
                                          int kp, int tid = -1, int nth = 0) {
@@ -67,8 +67,9 @@ __device__ __forceinline__ void gather_x(double* dst, int ld, const int* __restr
     for (int u = 0; u < GU; ++u) {
       const int e = e0 + u * nth, k = e / NRP;
       const bool ok = e < tot && k < kc && e - k * NRP < nrhs;
-      i1[u] = ok ? __ldg(xi + k) : -1;
-      i2[u] = (ok && x2) ? __ldg(x2 + k) : -1;
+      // PLAIN: the index arrays were staged in shared memory (no read-only-path load)
+      i1[u] = ok ? (PLAIN ? xi[k] : __ldg(xi + k)) : -1;
+      i2[u] = (ok && x2) ? (PLAIN ? x2[k] : __ldg(x2 + k)) : -1;
     }
     double v[GU];
 #pragma unroll
@@ -196,7 +197,8 @@ __global__ void __launch_bounds__(SW_THREADS) gemv_gather_kernel(GemvArgs a, int
 // lane group reads one 32-byte sector per row, 8 loads in flight per lane), X is gathered into
 // shared memory chunk by chunk with a padded stride (conflict-free B fragments).
 template <int NRP, bool VEC>
-__global__ void __launch_bounds__(256, 4) gemv_dmma_kernel(GemvArgs a, int rpc, int kchunk, int batch_off) {
+__global__ void __launch_bounds__(256, 4) gemv_dmma_kernel(GemvArgs a, int rpc, int kchunk, int batch_off,
+                                                            int stage_idx) {
   extern __shared__ double xs[];
   // VEC: each lane loads A[r][k+2t .. k+2t+1] as one 16-byte load and uses the two halves as
   // the A fragments of two "virtual" k4 steps; B fragments follow the same k permutation.
@@ -227,13 +229,25 @@ __global__ void __launch_bounds__(256, 4) gemv_dmma_kernel(GemvArgs a, int rpc, 
 #pragma unroll
     for (int n = 0; n < NT; ++n) acc[i][n][0] = acc[i][n][1] = 0.0;
   pdl_trigger();
+  // stage_idx: the (static) gather indices go to shared memory before the launch wait, so after
+  // it the x gather is one dependent global load per element instead of two
+  int* sidx = reinterpret_cast<int*>(red + (size_t)(WK - 1) * WR * 32 * (4 * NT));
+  if (stage_idx) {
+    for (int k = tid; k < K; k += blockDim.x) {
+      sidx[k] = __ldg(xi + k);
+      sidx[K + k] = x2 ? __ldg(x2 + k) : -1;
+    }
+  }
   pdl_wait();
 
   for (int k0 = 0; k0 < K; k0 += kchunk) {
     const int kc = min(kchunk, K - k0);
     const int kcp = VEC ? (kc + 7) & ~7 : (kc + 3) & ~3;
     __syncthreads();
-    gather_x<NRP, 4>(xs, XLD, xi + k0, x2 ? x2 + k0 : nullptr, pool, nrhs, kc, kcp);
+    if (stage_idx)
+      gather_x<NRP, 4, true>(xs, XLD, sidx + k0, x2 ? sidx + K + k0 : nullptr, pool, nrhs, kc, kcp);
+    else
+      gather_x<NRP, 4>(xs, XLD, xi + k0, x2 ? x2 + k0 : nullptr, pool, nrhs, kc, kcp);
     __syncthreads();
     if (VEC) {
       const int step = WK * 8;
@@ -780,17 +794,24 @@ static void launch_dmma(const GemvArgs& a, cudaStream_t s) {
   const int WR = rpc / 16, WK = 8 / WR;
   const size_t red = (size_t)(WK - 1) * WR * 32 * (4 * (NRP / 8));
   const int xld = vec ? NRP + 2 : NRP + 4;
-  int kchunk = (int)((48 * 1024 / 8 - red) / xld) & ~7;
+  static int stage_env = -1;  // HPS_STAGE_IDX=0: gather indices read after the launch wait
+  if (stage_env < 0) {
+    const char* e = getenv("HPS_STAGE_IDX");
+    stage_env = e ? atoi(e) : 1;
+  }
+  const int stage = stage_env && a.K <= 1024;
+  const size_t idx_doubles = stage ? ((size_t)2 * a.K * sizeof(int) + 7) / 8 : 0;
+  int kchunk = (int)((48 * 1024 / 8 - red - idx_doubles) / xld) & ~7;
   const int k8 = (a.K + 7) & ~7;
   if (kchunk > k8) kchunk = k8;
-  const size_t smem = sizeof(double) * ((size_t)kchunk * xld + red);
+  const size_t smem = sizeof(double) * ((size_t)kchunk * xld + red + idx_doubles);
   const int gx = (a.R + rpc - 1) / rpc;
   for (int off = 0; off < a.nitems; off += 65535) {
     dim3 grid(gx, min(65535, a.nitems - off));
     if (vec)
-      launch_k(gemv_dmma_kernel<NRP, true>, grid, dim3(256), smem, s, a, rpc, kchunk, off);
+      launch_k(gemv_dmma_kernel<NRP, true>, grid, dim3(256), smem, s, a, rpc, kchunk, off, stage);
     else
-      launch_k(gemv_dmma_kernel<NRP, false>, grid, dim3(256), smem, s, a, rpc, kchunk, off);
+      launch_k(gemv_dmma_kernel<NRP, false>, grid, dim3(256), smem, s, a, rpc, kchunk, off, stage);
   }
 }
 
