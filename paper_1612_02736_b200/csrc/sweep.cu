@@ -387,12 +387,25 @@ __global__ void __launch_bounds__(256) gemv_dmma_multi_kernel(GemvArgs a) {
   const int R = a.R, K = a.K, nrhs = a.nrhs;
   const int kp = (K + 3) & ~3;
   double* xs = xsm + (size_t)grp * kp * XLD;
+  // per-group index slice after all the x slices: [2][kp] ints, staged before the launch wait
+  int* sidx = reinterpret_cast<int*>(xsm + (size_t)IPC * kp * XLD) + (size_t)grp * 2 * kp;
   pdl_trigger();
+  const bool live = item < a.nitems;
+  const int* xi = a.xidx + (long long)(live ? item : 0) * a.xstride;
+  const int* x2 = a.x2idx ? a.x2idx + (long long)(live ? item : 0) * a.xstride : nullptr;
+  const int gtid = (int)threadIdx.x - grp * GW * 32;
+  if (live)
+    for (int k = gtid; k < K; k += GW * 32) {
+      sidx[k] = __ldg(xi + k);
+      sidx[kp + k] = x2 ? __ldg(x2 + k) : -1;
+    }
   pdl_wait();
-  if (item >= a.nitems) return;  // whole group
-  const int* xi = a.xidx + (long long)item * a.xstride;
-  const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
-  gather_x<NRP, 4>(xs, XLD, xi, x2, a.pool, nrhs, K, kp, (int)threadIdx.x - grp * GW * 32, GW * 32);
+  if (!live) return;  // whole group
+  if (GW == 1)
+    __syncwarp();
+  else
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(GW * 32) : "memory");
+  gather_x<NRP, 4, true>(xs, XLD, sidx, x2 ? sidx + kp : nullptr, a.pool, nrhs, K, kp, gtid, GW * 32);
   if (GW == 1)
     __syncwarp();
   else
@@ -474,7 +487,8 @@ static bool launch_dmma_multi(const GemvArgs& a, cudaStream_t s) {
   // downward steps of the deepest levels (R <= 32: one launch instead of two; 8192 items 232 ->
   // 123 us); slower for the upward steps, whose rows the 8 warps of a CTA split better
   if (!on || a.mode2 != 3 || a.aidx || a.R > 32) return false;
-  const size_t per_item = sizeof(double) * (size_t)((a.K + 3) & ~3) * (NRP + 4);
+  const size_t per_item = sizeof(double) * (size_t)((a.K + 3) & ~3) * (NRP + 4) +
+                          sizeof(int) * 2 * (size_t)((a.K + 3) & ~3);
   int ipc = 1;
   while (ipc < 8 && (long long)a.nitems / (2 * ipc) >= 2 * 148 && per_item * 2 * ipc <= 96 * 1024) ipc *= 2;
   if (ipc == 1 || a.R > 16 * 8 * 4) return false;  // one item per CTA: the kernel above
