@@ -516,7 +516,8 @@ static bool launch_dmma_multi(const GemvArgs& a, cudaStream_t s) {
 // lanes), 8 independent loads in flight per lane, group-wide shuffle reduction.
 // Scalar accumulation of columns [kb, ke) of RB rows: lane kl of an L-lane group takes columns
 // kb + kl + t*L, U loads per row in flight.
-template <int NR, int RB, int U>
+// SA: the rows live in shared memory (staged by a bulk copy), plain loads instead of __ldg
+template <int NR, int RB, int U, bool SA = false>
 __device__ __forceinline__ void dot_cols(double (&acc)[RB][NR], const double* const (&row)[RB],
                                          const bool (&live)[RB], int kb, int ke, int L, int kl,
                                          const double* xs) {
@@ -526,7 +527,7 @@ __device__ __forceinline__ void dot_cols(double (&acc)[RB][NR], const double* co
 #pragma unroll
     for (int q = 0; q < RB; ++q)
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[q][u] = live[q] ? __ldg(row[q] + k + u * L) : 0.0;
+      for (int u = 0; u < U; ++u) v[q][u] = live[q] ? (SA ? row[q][k + u * L] : __ldg(row[q] + k + u * L)) : 0.0;
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -539,7 +540,7 @@ __device__ __forceinline__ void dot_cols(double (&acc)[RB][NR], const double* co
   for (; k < ke; k += L) {
 #pragma unroll
     for (int q = 0; q < RB; ++q) {
-      const double v = live[q] ? __ldg(row[q] + k) : 0.0;
+      const double v = live[q] ? (SA ? row[q][k] : __ldg(row[q] + k)) : 0.0;
 #pragma unroll
       for (int j = 0; j < NR; ++j) acc[q][j] = fma(v, xs[k * NR + j], acc[q][j]);
     }
@@ -547,11 +548,11 @@ __device__ __forceinline__ void dot_cols(double (&acc)[RB][NR], const double* co
 }
 
 // ksplit < K (mode2 = 3): the partial sum over columns [0, ksplit) is also stored at o2idx[r].
-template <int NR, bool VEC, int RB = 2, int U = 4>
+template <int NR, bool VEC, int RB = 2, int U = 4, bool SA = false>
 __device__ __forceinline__ void rows_dot(const double* __restrict__ A, long long lda, int R, int r0, int r1,
                                          int K, int L, const double* xs, const int* aidx, const int* oidx,
                                          double* pool, int nrhs, double* ys, int ksplit = 1 << 30,
-                                         const int* o2idx = nullptr, int warp = -1, int nw = 0) {
+                                         const int* o2idx = nullptr, int warp = -1, int nw = 0, int arow0 = 0) {
   // each warp streams RB row groups at once (RB x U independent loads in flight per lane);
   // (warp, nw): this warp's index in the row-processing group (default: the whole CTA)
   const int lane = threadIdx.x & 31;
@@ -569,13 +570,13 @@ __device__ __forceinline__ void rows_dot(const double* __restrict__ A, long long
     for (int q = 0; q < RB; ++q) {
       const int r = rb + q * G + sub;
       live[q] = r < r1;
-      row[q] = A + (long long)(live[q] ? r : r0) * lda;
+      row[q] = A + (long long)((live[q] ? r : r0) - arow0) * lda;  // arow0: first row held at A
 #pragma unroll
       for (int j = 0; j < NR; ++j) acc[q][j] = accw[q][j] = 0.0;
     }
     if (split) {
-      dot_cols<NR, RB, U>(accw, row, live, 0, ksplit, L, kl, xs);
-      dot_cols<NR, RB, U>(acc, row, live, ksplit, K, L, kl, xs);
+      dot_cols<NR, RB, U, SA>(accw, row, live, 0, ksplit, L, kl, xs);
+      dot_cols<NR, RB, U, SA>(acc, row, live, ksplit, K, L, kl, xs);
 #pragma unroll
       for (int o = L >> 1; o > 0; o >>= 1)
 #pragma unroll
@@ -611,7 +612,7 @@ __device__ __forceinline__ void rows_dot(const double* __restrict__ A, long long
         }
       }
     } else {
-      dot_cols<NR, RB, U>(acc, row, live, 0, K, L, kl, xs);
+      dot_cols<NR, RB, U, SA>(acc, row, live, 0, K, L, kl, xs);
     }
 #pragma unroll
     for (int o = L >> 1; o > 0; o >>= 1)
@@ -644,10 +645,19 @@ __device__ __forceinline__ void rows_dot(const double* __restrict__ A, long long
 __host__ __device__ inline int lanes_for(int K) { return K <= 16 ? 4 : (K <= 48 ? 8 : (K <= 128 ? 16 : 32)); }
 
 // One work unit of a sweep step: item `item`, row chunk `chunk` of `nchunks` (rows_per_cta rows).
-template <int NR, bool VEC, int RB = 2, int U = 4, bool PDL = false>
+__device__ __forceinline__ uint32_t sw_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+// Shared-memory tile of the unit's operator rows (SA): doubles reserved in front of x
+__host__ __device__ inline int sa_tile_doubles(int rows, int ld) { return ((rows * ld + 2) + 1) & ~1; }
+
+template <int NR, bool VEC, int RB = 2, int U = 4, bool PDL = false, bool SA = false>
 __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chunk, int nchunks, int rows_per_cta,
                                            double* sm, int pf_rows = 1 << 30) {
-  double* xs = sm;                        // K x NR
+  // SA: the unit's operator rows (one contiguous range) are bulk-copied into shared memory
+  // BEFORE the launch wait (operators are static), so the dot products after it read on-chip
+  const int tdoubles = SA ? sa_tile_doubles(rows_per_cta, a.A.ld) : 0;
+  double* tile = sm;
+  double* xs = sm + tdoubles;             // K x NR
   double* ys = xs + (size_t)a.K * NR;     // R x NR (chain mode)
   const int K = a.K, nrhs = a.nrhs;
   const int* xi = a.xidx + (long long)item * a.xstride;
@@ -656,9 +666,28 @@ __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chun
   const double* Ai = a.A.get(item);
   const int r0 = chunk * rows_per_cta;
   const int r1 = min(a.R, r0 + rows_per_cta);
+  __shared__ __align__(8) uint64_t sa_bar;
+  int shift = 0;
+  if (SA) {
+    const uintptr_t src = reinterpret_cast<uintptr_t>(Ai + (long long)r0 * a.A.ld);
+    const uintptr_t s0 = src & ~(uintptr_t)15;
+    const uintptr_t s1 = (reinterpret_cast<uintptr_t>(Ai + (long long)(r1 - 1) * a.A.ld + K) + 15) & ~(uintptr_t)15;
+    shift = (int)((src - s0) / 8);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sw_smem(&sa_bar)));
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sw_smem(&sa_bar)),
+                   "r"((unsigned)(s1 - s0)) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+              sw_smem(tile)),
+          "l"(s0), "r"((unsigned)(s1 - s0)), "r"(sw_smem(&sa_bar))
+          : "memory");
+    }
+  }
   // start streaming this unit's operator rows into L2 while x is gathered (the first pf_rows:
   // a grid's worth of prefetches must fit in L2 or it evicts rows before they are used)
-  for (int r = r0 + threadIdx.x; r < min(r1, r0 + pf_rows); r += blockDim.x) {
+  for (int r = r0 + threadIdx.x; r < min(r1, r0 + (SA ? 0 : pf_rows)); r += blockDim.x) {
     const double* rp = Ai + (long long)r * a.A.ld;
     const uintptr_t lo = reinterpret_cast<uintptr_t>(rp) & ~(uintptr_t)15;
     const uintptr_t hi = (reinterpret_cast<uintptr_t>(rp + K) + 15) & ~(uintptr_t)15;
@@ -691,11 +720,21 @@ __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chun
     gather_x<NR>(xs, NR, xi, x2, pool, nrhs, K, K);
   }
   __syncthreads();
-  rows_dot<NR, VEC, RB, U>(Ai, a.A.ld, a.R, r0, r1, K, lanes_for(K), xs,
-                           a.aidx ? a.aidx + (long long)item * a.ostride : nullptr,
-                           a.oidx + (long long)item * a.ostride, a.pool, nrhs, a.mode2 == 2 ? ys : nullptr,
-                           a.mode2 == 3 ? a.K2 : 1 << 30,
-                           a.mode2 == 3 ? a.o2idx + (long long)item * a.ostride : nullptr);
+  if (SA)
+    asm volatile(
+        "{\n"
+        ".reg .pred P;\n"
+        "SAW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n"
+        "@!P bra SAW_%=;\n"
+        "}\n" ::"r"(sw_smem(&sa_bar))
+        : "memory");
+  rows_dot<NR, VEC, RB, U, SA>(SA ? tile + shift : Ai, a.A.ld, a.R, r0, r1, K, lanes_for(K), xs,
+                               a.aidx ? a.aidx + (long long)item * a.ostride : nullptr,
+                               a.oidx + (long long)item * a.ostride, a.pool, nrhs, a.mode2 == 2 ? ys : nullptr,
+                               a.mode2 == 3 ? a.K2 : 1 << 30,
+                               a.mode2 == 3 ? a.o2idx + (long long)item * a.ostride : nullptr, -1, 0,
+                               SA ? r0 : 0);
   if (a.mode2 == 1) {
     // tail stage rows split evenly over the row chunks of this item
     const int per = (a.R2 + nchunks - 1) / nchunks;
@@ -711,11 +750,11 @@ __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chun
   }
 }
 
-template <int NR, bool VEC, int RB = 2, int U = 4>
+template <int NR, bool VEC, int RB = 2, int U = 4, bool SA = false>
 __global__ void __launch_bounds__(256) sweep_kernel(GemvArgs a, int rows_per_cta, int batch_off, int pf_rows) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   pdl_trigger();
-  sweep_unit<NR, VEC, RB, U, true>(a, blockIdx.y + batch_off, blockIdx.x, gridDim.x, rows_per_cta, sm, pf_rows);
+  sweep_unit<NR, VEC, RB, U, true, SA>(a, blockIdx.y + batch_off, blockIdx.x, gridDim.x, rows_per_cta, sm, pf_rows);
 }
 
 // Several small items per CTA (deep tree levels: thousands of 15..60-row items): the CTA's warps
@@ -940,8 +979,20 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
   const long long cta_bytes = 8LL * a.K * rows;
   const long long cap = pf_kb >= 0 ? pf_kb * 1024 : (cta_bytes <= 160 * 1024 ? cta_bytes : 16 * 1024);
   const int pf_rows = (int)(cap / (8LL * a.K));
+  // SA: small operator tiles (latency-bound parent levels) go to shared memory by bulk copy
+  static int sa_kb = -1;  // HPS_SA_KB: largest tile staged this way (0 = off)
+  if (sa_kb < 0) {
+    const char* e = getenv("HPS_SA_KB");
+    sa_kb = e ? atoi(e) : 32;
+  }
+  const size_t sa_bytes = sizeof(double) * (size_t)sa_tile_doubles(rows, a.A.ld);
+  const bool sa = variant == 0 && sa_kb > 0 && sa_bytes <= (size_t)sa_kb * 1024 && smem + sa_bytes <= 48 * 1024;
   for (int off = 0; off < a.nitems; off += 65535) {
     dim3 grid(gx, min(65535, a.nitems - off));
+    if (sa) {
+      launch_k(sweep_kernel<NR, false, 2, 4, true>, grid, dim3(256), smem + sa_bytes, s, a, rows, off, pf_rows);
+      continue;
+    }
     switch (variant) {
       case 1: launch_k(sweep_kernel<NR, false, 1, 8>, grid, dim3(256), smem, s, a, rows, off, pf_rows); break;
       case 2: launch_k(sweep_kernel<NR, true, 1, 4>, grid, dim3(256), smem, s, a, rows, off, pf_rows); break;
