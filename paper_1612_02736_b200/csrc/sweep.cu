@@ -916,7 +916,7 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
     static int mink = -1;
     if (mink < 0) {
       const char* e = getenv("HPS_GATHER_MINK");
-      mink = e ? atoi(e) : 129;
+      mink = e ? atoi(e) : 1 << 30;  // default: the staged-x kernel for every step whose x fits
     }
     if (old && a.mode2 == 0 && a.K >= mink) return false;
     if (old && a.mode2 == 3 && a.K >= mink && getenv("HPS_SPLIT3_GATHER")) return false;
