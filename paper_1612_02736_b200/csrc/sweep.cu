@@ -983,7 +983,7 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
   static int sa_kb = -1;  // HPS_SA_KB: largest tile staged this way (0 = off)
   if (sa_kb < 0) {
     const char* e = getenv("HPS_SA_KB");
-    sa_kb = e ? atoi(e) : 32;
+    sa_kb = e ? atoi(e) : 40;
   }
   const size_t sa_bytes = sizeof(double) * (size_t)sa_tile_doubles(rows, a.A.ld);
   const bool sa = variant == 0 && sa_kb > 0 && sa_bytes <= (size_t)sa_kb * 1024 && smem + sa_bytes <= 48 * 1024;
