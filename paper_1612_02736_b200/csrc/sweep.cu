@@ -761,18 +761,40 @@ __global__ void __launch_bounds__(256) sweep_kernel(GemvArgs a, int rows_per_cta
 // are split into IPC groups of 256/IPC threads, each group gathers its item's x into its own slice
 // of shared memory (named barrier per group) and streams the item's rows. One wave of CTAs covers
 // the level instead of several waves of one-item CTAs. Single row chunk per item; mode2 0 or 3.
-template <int NR, int IPC>
+template <int NR, int IPC, bool SA = false>
 __global__ void __launch_bounds__(256) sweep_multi_kernel(GemvArgs a, int batch_off, int pf_rows) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   constexpr int GT = 256 / IPC;
   const int grp = threadIdx.x / GT, gtid = threadIdx.x % GT;
   const int item = (blockIdx.x + batch_off) * IPC + grp;
   const int K = a.K, nrhs = a.nrhs;
+  // SA: per-group operator tiles (whole item, bulk copy before the launch wait) after the x slices
+  const int tdoubles = SA ? sa_tile_doubles(a.R, a.A.ld) : 0;
+  const size_t xall = ((size_t)IPC * K * NR + 1) & ~(size_t)1;
   double* xs = sm + (size_t)grp * K * NR;
+  double* tile = sm + xall + (size_t)grp * tdoubles;
+  __shared__ __align__(8) uint64_t sa_bars[IPC];
   pdl_trigger();
   const bool live = item < a.nitems;
   const double* Ai = live ? a.A.get(item) : nullptr;
-  if (live) {
+  int shift = 0;
+  if (SA && live) {
+    const uintptr_t src = reinterpret_cast<uintptr_t>(Ai);
+    const uintptr_t s0 = src & ~(uintptr_t)15;
+    const uintptr_t s1 = (reinterpret_cast<uintptr_t>(Ai + (long long)(a.R - 1) * a.A.ld + K) + 15) & ~(uintptr_t)15;
+    shift = (int)((src - s0) / 8);
+    if (gtid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sw_smem(&sa_bars[grp])));
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sw_smem(&sa_bars[grp])),
+                   "r"((unsigned)(s1 - s0)) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                       sw_smem(tile)),
+                   "l"(s0), "r"((unsigned)(s1 - s0)), "r"(sw_smem(&sa_bars[grp]))
+                   : "memory");
+    }
+  }
+  if (live && !SA) {
     for (int r = gtid; r < min(a.R, pf_rows); r += GT) {
       const double* rp = Ai + (long long)r * a.A.ld;
       const uintptr_t lo = reinterpret_cast<uintptr_t>(rp) & ~(uintptr_t)15;
@@ -809,7 +831,16 @@ __global__ void __launch_bounds__(256) sweep_multi_kernel(GemvArgs a, int batch_
     __syncwarp();
   else
     asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(GT) : "memory");
-  rows_dot<NR, false>(Ai, a.A.ld, a.R, 0, a.R, K, lanes_for(K), xs,
+  if (SA)
+    asm volatile(
+        "{\n"
+        ".reg .pred P;\n"
+        "SMW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n"
+        "@!P bra SMW_%=;\n"
+        "}\n" ::"r"(sw_smem(&sa_bars[grp]))
+        : "memory");
+  rows_dot<NR, false, 2, 4, SA>(SA ? tile + shift : Ai, a.A.ld, a.R, 0, a.R, K, lanes_for(K), xs,
                       a.aidx ? a.aidx + (long long)item * a.ostride : nullptr,
                       a.oidx + (long long)item * a.ostride, a.pool, nrhs, nullptr,
                       a.mode2 == 3 ? a.K2 : 1 << 30, a.mode2 == 3 ? a.o2idx + (long long)item * a.ostride : nullptr,
@@ -946,19 +977,35 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
       min_ctas = e ? atoi(e) : 2 * 148;
     }
     int ipc = 1;
+    static int msa = -1;  // HPS_MULTI_SA=0: no shared-memory operator tiles in the multi-item kernel
+    if (msa < 0) {
+      const char* e = getenv("HPS_MULTI_SA");
+      msa = e ? atoi(e) : 1;
+    }
+    const size_t tile = sizeof(double) * (size_t)sa_tile_doubles(a.R, a.A.ld);
+    const bool sa = msa && a.A.ptrs == nullptr && tile <= 16 * 1024;
+    const size_t per_item = smem + (sa ? tile : 0);
     if (multi && gx == 1 && (a.mode2 == 0 || a.mode2 == 3)) {
-      // next ipc: the level still gives min_ctas CTAs, x fits, and the group's warps cover the
-      // item's rows in at most 4 passes (warps x row groups per warp x 2 rows)
-      while (ipc < 8 && (long long)a.nitems / (2 * ipc) >= min_ctas && smem * 2 * ipc <= 48 * 1024 &&
+      // next ipc: the level still gives min_ctas CTAs, x (and the tiles) fit, and the group's
+      // warps cover the item's rows in at most 4 passes (warps x row groups per warp x 2 rows)
+      while (ipc < 8 && (long long)a.nitems / (2 * ipc) >= min_ctas && per_item * 2 * ipc + 16 <= 48 * 1024 &&
              a.R <= (8 / (2 * ipc)) * (32 / lanes_for(a.K)) * 2 * 4)
         ipc *= 2;
     }
     if (ipc > 1) {
       const long long ctas = (a.nitems + ipc - 1) / ipc;
       const int pf_rows = 1 << 30;
+      const size_t sm2 = sa ? (((size_t)ipc * a.K * NR + 1) & ~(size_t)1) * sizeof(double) + tile * ipc : smem * ipc;
       for (long long off = 0; off < ctas; off += 2147483647LL) {
         const dim3 grid((unsigned)ctas);
-        const size_t sm2 = smem * ipc;
+        if (sa) {
+          switch (ipc) {
+            case 2: launch_k(sweep_multi_kernel<NR, 2, true>, grid, dim3(256), sm2, s, a, 0, pf_rows); break;
+            case 4: launch_k(sweep_multi_kernel<NR, 4, true>, grid, dim3(256), sm2, s, a, 0, pf_rows); break;
+            default: launch_k(sweep_multi_kernel<NR, 8, true>, grid, dim3(256), sm2, s, a, 0, pf_rows); break;
+          }
+          continue;
+        }
         switch (ipc) {
           case 2: launch_k(sweep_multi_kernel<NR, 2>, grid, dim3(256), sm2, s, a, 0, pf_rows); break;
           case 4: launch_k(sweep_multi_kernel<NR, 4>, grid, dim3(256), sm2, s, a, 0, pf_rows); break;
