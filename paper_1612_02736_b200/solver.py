@@ -411,7 +411,11 @@ class FactorizedSolver:
         pool = prog["pool"]
         N = self.plan.n_gauss
         s = _stream_ptr()
-        pool[:2 * N].zero_()
+        if not down:
+            # upward pass only: u must read zero (reference solver.py:418-425). A full solve
+            # needs no clearing: every u row is written (root exterior by the Dirichlet copy,
+            # each J3 set by its parent) and w rows outside the J3 sets are never written
+            pool[:2 * N].zero_()
         for step in prog["up"]:
             _ext.check(lib.hps_sweep_gemv(step, s), "upward sweep")
         if not down:
