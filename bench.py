@@ -321,7 +321,7 @@ def run_ours(args, rank, ws):
                             device="cuda").contiguous()
     g_dev = torch.as_tensor(np.repeat(g_host.reshape(-1, 1), nrhs, axis=1), device="cuda").contiguous()
     prog = solver._program(nrhs)
-    launches_per_step = len(prog["up"]) + len(prog["down"])
+    launches_per_step = len(prog["up"]) + len(prog["down"]) + 1  # + the Dirichlet copy
 
     for _ in range(args.warmup):
         solver.solve_device(f_dev, g_dev)

@@ -423,8 +423,17 @@ class FactorizedSolver:
                 _ext.check(lib.hps_sweep_gemv(step, s), "upward sweep (w3)")
             return
         down_steps = prog["down"] if leaves_down else prog["down"][:-len(self.leaf_groups)]
+        # the Dirichlet copy onto u's root exterior runs on a forked stream (nothing in the
+        # program reads it: readers take the f rows), joined before the program ends
+        cur = torch.cuda.current_stream()
+        side = prog.get("f_stream")
+        if side is None:
+            side = prog["f_stream"] = torch.cuda.Stream()
+        side.wait_stream(cur)
+        _ext.check(lib.hps_sweep_gemv(prog["copy_f"], side.cuda_stream), "Dirichlet copy")
         for step in down_steps:
             _ext.check(lib.hps_sweep_gemv(step, s), "downward sweep")
+        cur.wait_stream(side)
 
     def _graph(self, prog, key, **kw):
         """CUDA graph of _steps(prog, **kw), captured on first use."""
@@ -636,7 +645,17 @@ class FactorizedSolver:
         copy_f = dict(nitems=root_ext.size, R=1, K=1, A=_ext.mat(one, 0, 1),
                       xidx=(f_rows + np.arange(root_ext.size))[:, None], oidx=(lay["U"] + root_ext)[:, None],
                       x2idx=None, aidx=None, mode2=0, R2=0, K2=0, A2=None, o2idx=None, a2idx=None)
-        down = [copy_f] + down
+        # every reader of the root exterior reads the f rows directly, so the copy onto u is off
+        # the critical path (a forked branch of the program, joined at its end; _steps)
+        lut = np.full(scratch[0] + 1, -1, dtype=np.int64)
+        lut[lay["U"] + root_ext] = f_rows + np.arange(root_ext.size)
+        for sp in down:
+            for k in ("xidx", "x2idx", "aidx"):
+                arr = sp.get(k)
+                if arr is None:
+                    continue
+                t = np.where(arr >= 0, lut[np.clip(arr, 0, None)], -1)
+                sp[k] = np.where(t >= 0, t, arr)
         pool = torch.zeros((scratch[0], nrhs), dtype=torch.float64, device=self.device)
 
         def build(spec):
@@ -655,6 +674,7 @@ class FactorizedSolver:
         ng = len(self.leaf_groups)
         up = [build(s_) for s_ in up]
         down = [build(s_) for s_ in down]
+        copy_f = build(copy_f)
         # leaf downward step as leaf-range launches (host-API path, _run_overlapped)
         leaf_chunks = []
         for gi, grp in enumerate(self.leaf_groups):
@@ -674,7 +694,7 @@ class FactorizedSolver:
                 leaf_chunks.append((cb, grp.first_row + i0, grp.first_row + i1))
         wonly = [build(s_) for s_ in wonly]
         f_in = pool[f_rows:f_rows + root_ext.size]
-        prog = {"pool": pool, "up": up, "down": down, "wonly": wonly, "keep": keep, "f_in": f_in,
+        prog = {"pool": pool, "up": up, "down": down, "wonly": wonly, "keep": keep, "f_in": f_in, "copy_f": copy_f,
                 "leaf_chunks": leaf_chunks,
                 "graph": None, "patches": patches}
         self._sweeps[nrhs] = prog
