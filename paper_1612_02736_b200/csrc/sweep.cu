@@ -983,7 +983,7 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
       msa = e ? atoi(e) : 1;
     }
     const size_t tile = sizeof(double) * (size_t)sa_tile_doubles(a.R, a.A.ld);
-    const bool sa = msa && a.A.ptrs == nullptr && tile <= 16 * 1024;
+    const bool sa = msa && a.A.ptrs == nullptr && tile <= 40 * 1024;  // larger items fall back to ipc = 1
     const size_t per_item = smem + (sa ? tile : 0);
     if (multi && gx == 1 && (a.mode2 == 0 || a.mode2 == 3)) {
       // next ipc: the level still gives min_ctas CTAs, x (and the tiles) fit, and the group's
