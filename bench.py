@@ -185,6 +185,21 @@ def barrier(ws):
             dist.barrier()
 
 
+def config_dict(args, desc, nrhs, ncheb, ops_bytes, ws):
+    """The `config` object, identical in both arms (the driver compares them)."""
+    return {"workload": desc, "nrhs": nrhs, "N_cheb": ncheb,
+            "l2": "operators (%.2f GB) exceed the 126 MB L2; no flush needed" % (ops_bytes / 1e9),
+            "parallelism": f"replicas over RHS x{ws}" if ws > 1 else "1 GPU"}
+
+
+def leaf_dict(tree, table_rows):
+    """{leaf id: (m,) interior tabulation} in the reference's g convention (solver.py:241-253),
+    built once outside any timed region; table_rows = rows of a (n_leaves, m) table in the
+    solver's leaf-row order, paired with solver._leaf_ids."""
+    ids, table = table_rows
+    return {int(n): table[r] for r, n in enumerate(ids)}
+
+
 # --------------------------------------------------------------------------- CPU reference arm
 
 def cpu_solve_rate(tree, spec, p, q, plan, reps=1, threads=None):
@@ -259,12 +274,14 @@ def run_reference(args, rank, ws):
     per = el / timed
     val = ncheb * args.nrhs / (per * args.nrhs) / 1e6
     lf, mf = canonical_build_flops(tree, plan, p, q)
+    sb_ops, _ = solve_bytes(tree, plan, p, q, args.nrhs)
     line = {"impl": "reference", "metric": "HPS solve Mpts/s per RHS", "value": round(val, 4),
             "unit": "Mpts/s per RHS", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(per * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded manufactured solution, SURVEY.md 8d)",
-            "config": {"workload": desc, "nrhs": 1, "N_cheb": ncheb},
-            "cpu_baseline": {"value": round(val, 4), "unit": "Mpts/s per RHS", "cores": th, "kind": "port",
+            "config": config_dict(args, desc, args.nrhs, ncheb, sb_ops, ws),
+            "cpu_baseline": {"value": round(val, 4), "unit": "Mpts/s per RHS", "cores": th,
+                             "host_cores": os.cpu_count(), "kind": "port",
                              "sample": f"full workload; oracle/hps_oracle.py numpy/scipy, OPENBLAS threads={th} "
                                        f"(best of a 1/4/nproc sweep), {timed} timed solves (of K={args.steps}; "
                                        f"capped at ~90 s of CPU time)"},
@@ -275,6 +292,122 @@ def run_reference(args, rank, ws):
 
 
 # --------------------------------------------------------------------------- GPU arm
+
+def _node_depths(tree):
+    depth = {tree.root: 0}
+    stack = [tree.root]
+    while stack:
+        nid = stack.pop()
+        for c in tree.nodes[nid].children:
+            depth[c] = depth[nid] + 1
+            stack.append(c)
+    return depth
+
+
+def _merge_flops(plan, nid):
+    en = plan.node[nid]
+    m3, e = en.j3.size, en.ext_mergeorder.size
+    return (2.0 / 3.0) * m3 ** 3 + 2.0 * m3 * m3 * e + 2.0 * e * e * m3
+
+
+def build_largest(reps=2):
+    """North-star build target: FP64 tensor utilisation on the LARGEST batches,
+    config 3's 1,024-leaf p=32 leaf stage (one hps_leaf_build) and config 5's top merge levels
+    0-4 (31 merges, m3 up to 1,920). CUDA-event phase marks of build_stage(profile=True) around
+    exactly those ABI calls; canonical FLOPs of SURVEY.md 8d; best of `reps` timed builds after
+    one warm-up build."""
+    import torch
+    from paper_1612_02736_b200 import build_stage
+    from paper_1612_02736_b200.geometry import enumerate_gauss_nodes
+    out = {}
+    for cfg in (3, 5):
+        tree, spec, p, q, desc = make_config(cfg)
+        plan = enumerate_gauss_nodes(tree, q)
+        m, b, c, P = (p - 2) ** 2, 4 * q, 4 * (p - 1), p * p
+        nleaf = sum(1 for n in tree.nodes if n.is_leaf)
+        leaf_gf = nleaf * (2.0 * m ** 3 + 2.0 * m * c * b + 2.0 * m * m * b + 2.0 * b * P * b + 2.0 * b * m * m) / 1e9
+        depth = _node_depths(tree)
+        top = {d: sum(_merge_flops(plan, n) for n, dd in depth.items()
+                      if dd == d and not tree.nodes[n].is_leaf) / 1e9 for d in range(5)}
+        best = None
+        for r in range(reps + 1):
+            solver = build_stage(tree, spec, p, q, plan=plan, profile=True)
+            ph = solver.phase_ms
+            del solver
+            torch.cuda.synchronize()
+            leaf_ms = sum(ms for name, ms in ph if name.startswith("leaf-build"))
+            merge_ms = {d: sum(ms for name, ms in ph if name.startswith(f"merge d{d} ")) for d in range(5)}
+            if r == 0:
+                continue  # warm-up
+            if best is None or leaf_ms + sum(merge_ms.values()) < best[0] + sum(best[1].values()):
+                best = (leaf_ms, merge_ms)
+        leaf_ms, merge_ms = best
+        if cfg == 3:
+            out["config3_leaves"] = {
+                "what": f"{nleaf} leaves p=32 (m=900) in one hps_leaf_build", "gflop": round(leaf_gf, 1),
+                "ms": round(leaf_ms, 2), "tflops": round(leaf_gf / leaf_ms, 2),
+                "frac_fp64_peak": round(leaf_gf / leaf_ms / FP64_PEAK_TFLOPS, 4)}
+        else:
+            gf = sum(top.values())
+            ms = sum(merge_ms.values())
+            out["config5_top_merges"] = {
+                "what": "levels 0-4 (31 merges, m3 480-1920, e 1920-7680), hps_merge_build per level",
+                "gflop": round(gf, 1), "ms": round(ms, 2), "tflops": round(gf / ms, 2),
+                "frac_fp64_peak": round(gf / ms / FP64_PEAK_TFLOPS, 4),
+                "per_level": {str(d): {"gflop": round(top[d], 1), "ms": round(merge_ms[d], 2),
+                                       "frac_fp64_peak": round(top[d] / merge_ms[d] / FP64_PEAK_TFLOPS, 4)}
+                              for d in range(5)}}
+            out["config5_leaves"] = {
+                "what": f"{nleaf} leaves p=16 (m=196) in one hps_leaf_build", "gflop": round(leaf_gf, 1),
+                "ms": round(leaf_ms, 2), "tflops": round(leaf_gf / leaf_ms, 2),
+                "frac_fp64_peak": round(leaf_gf / leaf_ms / FP64_PEAK_TFLOPS, 4)}
+    out["fp64_peak_tflops"] = FP64_PEAK_TFLOPS
+    out["peak_source"] = "measured DMMA m8n8k4 (tools/fp64_peaks.cu, profiles/fp64_peaks_r01.jsonl)"
+    return out
+
+
+def timestep_config5(hbm_peak, nts=20, nrhs=16):
+    """North-star repeated workload: one backward-Euler step of config 5 (128x128 leaves, p=16,
+    dt=1e-3) for 16 RHS = hps_leaf_apply (g = u_n/dt, device-resident) + the graph-replayed
+    16-RHS solve. Bytes = canonical solve bytes at nrhs=16 (operators once + vectors) + the load
+    formation (read u_c[i_ci], write g: 2 m doubles per leaf per RHS)."""
+    import torch
+    from paper_1612_02736_b200 import build_stage
+    from paper_1612_02736_b200.geometry import count_chebyshev_dofs, enumerate_gauss_nodes
+    from paper_1612_02736_b200.timestepping import DeviceStepper
+    tree, spec, p, q, desc = make_config(5)
+    plan = enumerate_gauss_nodes(tree, q)
+    ncheb = count_chebyshev_dofs(tree, p)
+    solver = build_stage(tree, spec, p, q, plan=plan)
+    stp = DeviceStepper(solver, nrhs, 1.0 / float(spec.params["dt"]), 0.0)
+    from paper_1612_02736_b200 import problems
+    stp.set_state(torch.zeros_like(stp.leaf_tabulations()))
+    bpts = plan.coords[plan.node[tree.root].ext]
+    f16 = torch.as_tensor(np.repeat(problems.config5_dirichlet(bpts, 1e-3)[:, None], nrhs, axis=1),
+                          device="cuda").contiguous()
+    for _ in range(3):
+        stp.step(f16)
+    torch.cuda.synchronize()
+    t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0e.record()
+    for _ in range(nts):
+        stp.step(f16)
+    t1e.record()
+    torch.cuda.synchronize()
+    tper = t0e.elapsed_time(t1e) / 1e3 / nts
+    ops, vec = solve_bytes(tree, plan, p, q, nrhs)
+    m = (p - 2) ** 2
+    nleaf = solver._n_leaves
+    byts = ops + vec + 8.0 * nleaf * 2 * m * nrhs
+    del stp, solver
+    return {"workload": desc, "nrhs": nrhs, "ms_per_step": round(tper * 1e3, 4),
+            "Mpts_per_s_per_rhs": round(ncheb * nrhs / tper / 1e6, 1),
+            "trajectory_1000_steps_s": round(tper * 1000, 3),
+            "bytes_per_step": byts, "achieved_gbs": round(byts / tper / 1e9, 1),
+            "frac_hbm": round(byts / tper / 1e9 / hbm_peak, 4),
+            "what": "hps_leaf_apply (g = u_n/dt) + graph-replayed 16-RHS solve, CUDA events, "
+                    f"{nts} steps after 3 warm-up"}
+
 
 def run_ours(args, rank, ws):
     import torch
@@ -339,31 +472,6 @@ def run_ours(args, rank, ws):
     per = el / args.steps
     value = ncheb * nrhs * ws / per / 1e6
 
-    # ---- config 5: the repeated implicit step itself (BE load u_n/dt on device + solve), 16 RHS
-    timestep = None
-    if args.config == 5:
-        from paper_1612_02736_b200.timestepping import DeviceStepper
-        tr = 16
-        stp = DeviceStepper(solver, tr, 1.0 / float(spec.params["dt"]), 0.0)
-        stp.set_state(torch.zeros_like(stp.leaf_tabulations()))
-        f16 = torch.as_tensor(np.repeat(f_host[:, None], tr, axis=1), device="cuda").contiguous()
-        for _ in range(3):
-            stp.step(f16)
-        torch.cuda.synchronize()
-        nts = 20
-        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0e.record()
-        for _ in range(nts):
-            stp.step(f16)
-        t1e.record()
-        torch.cuda.synchronize()
-        tper = t0e.elapsed_time(t1e) / 1e3 / nts
-        timestep = {"nrhs": tr, "ms_per_step": round(tper * 1e3, 4),
-                    "Mpts_per_s_per_rhs": round(ncheb * tr / tper / 1e6, 1),
-                    "trajectory_1000_steps_s": round(tper * 1000, 3),
-                    "what": "hps_leaf_apply (g = u_n/dt) + graph-replayed 16-RHS solve, CUDA events"}
-        del stp
-
     # ---- dominant kernel: leaf downward sweep ([F|S] [g; u_ext]), timed alone on the stream
     lib = _ext.load()
     sptr = torch.cuda.current_stream().cuda_stream
@@ -384,17 +492,21 @@ def run_ours(args, rank, ws):
     kbytes = 8.0 * nleaf * (m * (m + b) + (m + b) * nrhs + (m + c_ext) * nrhs)
     achieved = kbytes / kt / 1e9
 
-    # ---- e2e through the public host API (host numpy in, host numpy out)
+    # ---- e2e through the public host API in the reference's own input convention: f as an
+    # array on the root exterior, g as a {leaf id: (m,)} mapping; host numpy in,
+    # host numpy out (SolveState.u, w, h_root, every leaf tabulation)
     g_tab = solver._leaf_table(None)
-    e2e_steps = max(1, min(args.steps, 10))
+    g_dict = leaf_dict(tree, (solver._leaf_ids, g_tab))
+    e2e_steps = max(1, min(args.steps, 20))
     for _ in range(max(args.warmup, 3)):
-        st = solver.solve(f=f_host, g=g_tab)
+        st = solver.solve(f=f_host, g=g_dict)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        st = solver.solve(f=f_host, g=g_tab)
+        st = solver.solve(f=f_host, g=g_dict)
     e2e_t = (time.perf_counter() - t0) / e2e_steps
     e2e_t = max_over_ranks(e2e_t, ws)
+    del st
     lay = solver._layout
     h2d = 8 * (root_ext.size + g_tab.size)
     # read back: u | w (2 N_gauss), h_root and the leaf tabulations (n_leaves x p^2)
@@ -408,7 +520,8 @@ def run_ours(args, rank, ws):
         splan = enumerate_gauss_nodes(stree, q)
         th = min(4, os.cpu_count() or 1)
         rate, tb, ts = cpu_solve_rate(stree, sspec, p, q, splan, reps=3, threads=th)
-        cpu = {"value": round(rate, 4), "unit": "Mpts/s per RHS", "cores": th, "kind": "port",
+        cpu = {"value": round(rate, 4), "unit": "Mpts/s per RHS", "cores": th, "host_cores": os.cpu_count(),
+               "kind": "port",
                "sample": f"{sdesc}: oracle build ({tb:.1f} s) + best of 3 solves ({ts * 1e3:.1f} ms), "
                          f"OPENBLAS threads={th}"}
 
@@ -426,9 +539,7 @@ def run_ours(args, rank, ws):
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(per * 1e3, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded manufactured solution / loads, SURVEY.md 8d; no dataset)",
-        "config": {"workload": desc, "nrhs": nrhs, "N_cheb": ncheb,
-                   "l2": "operators (%.2f GB) exceed the 126 MB L2; no flush needed" % (sb_ops / 1e9),
-                   "parallelism": f"replicas over RHS x{ws}" if ws > 1 else "1 GPU"},
+        "config": config_dict(args, desc, nrhs, ncheb, sb_ops, ws),
         "roofline": {"bound": "hbm", "kernel": "sweep_kernel (leaf downward sweep, [F|S][g;u_ge] + L u_ge)", "achieved": round(achieved, 1),
                      "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                      "algorithmic_bytes": kbytes,
@@ -451,8 +562,15 @@ def run_ours(args, rank, ws):
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
     }
-    if timestep:
-        line["timestep"] = timestep
+    if not args.no_extras and rank == 0:
+        # north-star targets beyond the headline metric, in their own
+        # clock-sampled region after the timed solve loop
+        del solver, prog
+        torch.cuda.empty_cache()
+        with ClockSampler(local) as clk2:
+            extra = {"build_largest": build_largest(), "timestep": timestep_config5(hbm_peak)}
+        extra["clocks"] = clk2.summary()
+        line["north_star"] = extra
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -467,6 +585,8 @@ def main():
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--nrhs", type=int, default=1)
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the north-star build/timestep measurements (config 3 and 5 builds)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank, ws = dist_init()

@@ -7,7 +7,7 @@ in hand-written sm_100a CUDA kernels behind the C ABI in include/hps_b200.h.
 """
 
 from .geometry import (BoxNode, DomainTree, MeshConformityError, MergePlan, MeshSpec, NodePlan, Rect,
-                       build_balanced_refined_tree, build_forest, build_mesh, build_uniform_tree,
+                       RefinementSpec, build_balanced_refined_tree, build_forest, build_mesh, build_uniform_tree,
                        count_chebyshev_dofs, enumerate_gauss_nodes, refine_near_point)
 from .model import CoefficientField, ProblemSpec, catalog, manufactured_spec
 from .solver import (FactorizedSolver, LeafSingularError, MergeSingularError, SolveState,
@@ -19,7 +19,7 @@ from .archive import ArchiveError, load_operators, persist_operators
 __version__ = "0.1.0"
 
 __all__ = [
-    "BoxNode", "DomainTree", "MeshConformityError", "MergePlan", "MeshSpec", "NodePlan", "Rect",
+    "BoxNode", "DomainTree", "MeshConformityError", "MergePlan", "MeshSpec", "NodePlan", "Rect", "RefinementSpec",
     "build_balanced_refined_tree", "build_forest", "build_mesh", "build_uniform_tree", "count_chebyshev_dofs",
     "enumerate_gauss_nodes", "refine_near_point", "CoefficientField", "ProblemSpec", "catalog",
     "manufactured_spec", "FactorizedSolver", "LeafSingularError", "MergeSingularError",

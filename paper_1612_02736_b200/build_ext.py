@@ -34,18 +34,48 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps if os.path.exists(d))
 
 
+OBJ = os.path.join(PKG, "_build")
+
+
+def _headers():
+    hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    return hs + [os.path.join(ROOT, "include", "hps_b200.h")]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile each source to an object (in parallel; a source is recompiled when it or any
+    header is newer than its object), then link the shared library."""
     if not force and up_to_date():
         return LIB
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"),
-           "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(OBJ, exist_ok=True)
+    hdr_t = max(os.path.getmtime(h) for h in _headers() if os.path.exists(h))
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+             "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include")]
+
+    def compile_one(src):
+        cu, obj = os.path.join(CSRC, src), os.path.join(OBJ, src.replace(".cu", ".o"))
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(cu), hdr_t):
+            return obj, None
+        res = subprocess.run([nvcc(), *flags, "-c", cu, "-o", obj + ".tmp"], capture_output=True, text=True)
+        if res.returncode != 0:
+            return obj, res.stdout + res.stderr
+        os.replace(obj + ".tmp", obj)
+        if verbose:
+            sys.stderr.write(res.stderr)
+        return obj, None
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    errs = [e for _, e in results if e]
+    if errs:
+        sys.stderr.write("\n".join(errs))
+        raise RuntimeError("nvcc failed building the HPS extension")
+    res = subprocess.run([nvcc(), *ARCH, "-shared", "-o", LIB + ".tmp", *[o for o, _ in results]],
+                         capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building the HPS extension")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc failed linking the HPS extension")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

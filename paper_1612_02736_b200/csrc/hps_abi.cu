@@ -1,4 +1,6 @@
 // extern "C" entry points (include/hps_b200.h) -> internal launchers.
+#include <cstdlib>
+
 #include "../../include/hps_b200.h"
 #include "hps_kernels.cuh"
 
@@ -212,6 +214,14 @@ static int to_gemv_args(const hps_gemv_batch* gb, GemvArgs* out) {
   a.o2idx = gb->o2idx;
   a.xstride = a.K;
   a.ostride = a.R;
+  // HPS_PRE_INDEX (read once per process, host side only): bit mask of the kernels that load
+  // their static gather indices before the programmatic-launch wait; a kernel argument, so no
+  // device-symbol copy (and no legacy-stream work) ever happens inside a launch path
+  static const int pre_mask = [] {
+    const char* e = getenv("HPS_PRE_INDEX");
+    return e ? atoi(e) : 15;
+  }();
+  a.pre_mask = pre_mask;
   if (a.mode2 && (!a.o2idx || a.R2 <= 0 || a.K2 <= 0 || (a.mode2 == 1 && a.K2 > a.K) ||
                   (a.mode2 == 2 && a.K2 != a.R) ||
                   (a.mode2 == 3 && (a.R2 != a.R || a.K2 >= a.K || a.aidx)) || a.mode2 > 3))

@@ -100,6 +100,8 @@ struct GemvArgs {
   const int* o2idx;  // [nitems][R2]
   long long xstride; // per-item stride of xidx/x2idx (default K) and of aidx/oidx (default R)
   long long ostride;
+  int pre_mask;      // which kernels load static gather indices before the launch wait
+                     // (bit mask, HPS_PRE_INDEX, set per launch by launch_gemv_gather)
 };
 int launch_gemv_gather(const GemvArgs& a, cudaStream_t s);
 // TMA-fed multi-RHS path for large leaf levels (sweep_tma.cu); false = not applicable

@@ -19,8 +19,7 @@ constexpr int SW_THREADS = 256;
 
 // 1: single-RHS kernels load their (static) gather indices before the programmatic-launch wait
 // (bit mask: 1 staged-x row kernel, 2 gather kernel, 4 multi-item kernel, 8 one-row kernel)
-static __device__ __constant__ int c_pre_index = 15;
-__device__ __forceinline__ bool pre_index(int bit = 1) { return (c_pre_index & bit) != 0; }
+#define pre_index(bit) ((a.pre_mask & (bit)) != 0)
 
 // every sweep launch carries the programmatic-serialization attribute (HPS_PDL=0 disables)
 static bool pdl_enabled() {
@@ -693,7 +692,7 @@ __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chun
     const uintptr_t hi = (reinterpret_cast<uintptr_t>(rp + K) + 15) & ~(uintptr_t)15;
     prefetch_l2_bulk(reinterpret_cast<const void*>(lo), (unsigned)(hi - lo));
   }
-  if (NR == 1 && PDL && K <= 2 * (int)blockDim.x && pre_index()) {
+  if (NR == 1 && PDL && K <= 2 * (int)blockDim.x && pre_index(1)) {
     // single RHS, short x: the gather indices are static, so they are loaded before the
     // programmatic-launch wait; after it only the pool rows remain on the critical path
     int i1[2], i2[2];
@@ -929,15 +928,6 @@ static int variant_of_env() {
 template <int NR>
 static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
   {
-    static bool pre_set = false;  // HPS_PRE_INDEX=0: gather indices after the launch wait
-    if (!pre_set) {
-      const char* e = getenv("HPS_PRE_INDEX");
-      const int v = e ? atoi(e) : 15;
-      cudaMemcpyToSymbol(c_pre_index, &v, sizeof(int));
-      pre_set = true;
-    }
-  }
-  {
     static int old = -1;
     if (old < 0) {
       const char* e = getenv("HPS_SWEEP_VARIANT");
@@ -988,7 +978,8 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
     if (multi && gx == 1 && (a.mode2 == 0 || a.mode2 == 3)) {
       // next ipc: the level still gives min_ctas CTAs, x (and the tiles) fit, and the group's
       // warps cover the item's rows in at most 4 passes (warps x row groups per warp x 2 rows)
-      while (ipc < 8 && (long long)a.nitems / (2 * ipc) >= min_ctas && per_item * 2 * ipc + 16 <= 48 * 1024 &&
+      // (+ the kernel's static shared memory: one 8-byte mbarrier per item, plus 16 B)
+      while (ipc < 8 && (long long)a.nitems / (2 * ipc) >= min_ctas && (per_item + 8) * 2 * ipc + 16 <= 48 * 1024 &&
              a.R <= (8 / (2 * ipc)) * (32 / lanes_for(a.K)) * 2 * 4)
         ipc *= 2;
     }
@@ -1033,7 +1024,8 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
     sa_kb = e ? atoi(e) : 40;
   }
   const size_t sa_bytes = sizeof(double) * (size_t)sa_tile_doubles(rows, a.A.ld);
-  const bool sa = variant == 0 && sa_kb > 0 && sa_bytes <= (size_t)sa_kb * 1024 && smem + sa_bytes <= 48 * 1024;
+  // (+ 64 B of static shared memory: the tile's mbarrier)
+  const bool sa = variant == 0 && sa_kb > 0 && sa_bytes <= (size_t)sa_kb * 1024 && smem + sa_bytes + 64 <= 48 * 1024;
   for (int off = 0; off < a.nitems; off += 65535) {
     dim3 grid(gx, min(65535, a.nitems - off));
     if (sa) {
@@ -1140,6 +1132,7 @@ int launch_gemv_gather(const GemvArgs& a, cudaStream_t s) {
     GemvArgs c{};
     c.nitems = a.nitems;
     c.nrhs = a.nrhs;
+    c.pre_mask = a.pre_mask;
     c.pool = a.pool;
     c.A = a.A2;
     c.R = a.R2;

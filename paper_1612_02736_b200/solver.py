@@ -18,9 +18,9 @@ Operators stay resident in HBM as torch tensors owned by the solver object.
 from __future__ import annotations
 
 import math
-import sys
+import threading
 import time
-import warnings
+import weakref
 from collections.abc import Mapping
 from dataclasses import dataclass, field
 
@@ -79,8 +79,34 @@ def _f64(a, dev):
     return _upload(np.ascontiguousarray(a, dtype=np.float64), dev)
 
 
+def _op_empty(shape, dev):
+    """Operator tensor with 16 bytes of slack past its last element: the sweep kernels stage
+    operator rows with 16-byte-granular bulk copies, which may round the end of the last row up
+    past an odd-length tensor."""
+    n = int(np.prod(shape))
+    return torch.empty(n + 2, dtype=torch.float64, device=dev)[:n].view(shape)
+
+
+def _op_f64(a, dev):
+    """Host operator -> device, with the same slack as _op_empty."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    t = _op_empty(a.shape, dev)
+    t.copy_(torch.from_numpy(a))
+    return t
+
+
 def _ptr_array(ptrs, dev):
     return _upload(np.ascontiguousarray(ptrs, dtype=np.int64), dev)
+
+
+class _HostLease:
+    """numpy base object for a lent page-locked result buffer (FactorizedSolver._out_buffers):
+    arrays built from it keep it alive, and its death returns the buffer to the ring."""
+
+    def __init__(self, t: torch.Tensor):
+        self._t = t
+        self.__array_interface__ = {"shape": (t.numel(),), "typestr": "<f8",
+                                    "data": (t.data_ptr(), False), "version": 3}
 
 
 class LeafSolutions(Mapping):
@@ -170,6 +196,10 @@ class FactorizedSolver:
         self.depth: dict = {}
         self._sweeps: dict = {}        # nrhs -> compiled sweep program
         self.events: dict = {}
+        # a built solver is immutable and serves concurrent solves (reference SPEC.md:421-422);
+        # the device vector pool and captured graphs are per solver, so host-API solves from
+        # several threads are serialised here and each one returns its own host arrays
+        self._lock = threading.RLock()
 
     # -- accounting -------------------------------------------------------------------------
     def leaf_memory_floats(self) -> int:
@@ -226,7 +256,7 @@ class FactorizedSolver:
             else:
                 ldx, xsrc, xstride = m3 + e, grp.xs, m3 * (m3 + e)
             n = len(grp.ids)
-            grp.y = torch.empty((n, e, m3), dtype=torch.float64, device=self.device)
+            grp.y = _op_empty((n, e, m3), self.device)
             _ext.check(lib.hps_gemm_batched(n, e, m3, m3, 1.0, _ext.mat(grp.tei, e * m3, m3),
                                             _ext.mat(xsrc, xstride, ldx), 0.0, _ext.mat(grp.y, e * m3, m3),
                                             None, 0, s), "solve operator Y = T_ei X")
@@ -254,19 +284,28 @@ class FactorizedSolver:
             if tuple(arr.shape) != (nl, m):
                 raise ValueError(f"load table has shape {tuple(arr.shape)}, expected ({nl}, {m})")
             return arr
-        out = np.empty((nl, m))
         if callable(g):
+            out = np.empty((nl, m))
             for grp in self.leaf_groups:
                 pts = self._interior_points(grp)
                 vals = np.asarray(g(pts.reshape(-1, 2)), dtype=float).reshape(len(grp.ids), m)
                 out[grp.first_row:grp.first_row + len(grp.ids)] = vals
             return out
-        for grp in self.leaf_groups:
-            for slot, nid in enumerate(grp.ids):
-                g_ci = np.asarray(g[nid], dtype=float)
-                if g_ci.shape != (m,):
-                    raise ValueError(f"leaf {nid} load has shape {g_ci.shape}, expected ({m},)")
-                out[grp.first_row + slot] = g_ci
+        if isinstance(g, LeafSolutions) and g._row is getattr(self, "_leaf_rowmap", None):
+            tab = np.asarray(g._table, dtype=float)  # a state's own g_tab: already leaf-row order
+            if tab.shape == (nl, m):
+                return tab
+        # mapping {leaf id: (m,)} (reference solver.py:246-252): one gather in leaf-row order
+        vals = [g[nid] for nid in self._leaf_ids]
+        try:
+            out = np.asarray(vals, dtype=float)
+        except ValueError:
+            out = None
+        if out is None or out.shape != (nl, m):
+            for nid, v in zip(self._leaf_ids, vals):
+                shp = np.shape(v)
+                if shp != (m,):
+                    raise ValueError(f"leaf {nid} load has shape {shp}, expected ({m},)")
         return out
 
     def _interior_points(self, grp):
@@ -298,6 +337,10 @@ class FactorizedSolver:
     def _solve_host(self, f, g, down=True) -> SolveState:
         fv = self._dirichlet(f) if down else None
         gt = self._leaf_table(g)
+        with self._lock:
+            return self._solve_host_locked(fv, gt, g, down)
+
+    def _solve_host_locked(self, fv, gt, g, down) -> SolveState:
         prog = self._program(1)
         lay, pool = self._layout, prog["pool"]
         N, P, nl = self.plan.n_gauss, self.p ** 2, self._n_leaves
@@ -310,7 +353,7 @@ class FactorizedSolver:
             gtab = gt.detach().cpu().numpy() if isinstance(gt, torch.Tensor) else np.asarray(gt)
             st.g_tab = self._leaf_view(gtab)
             return st
-        self._execute(prog, down=down)
+        self._execute(prog, phase="full" if down else "up")
         # D2H of the result regions only: U|W (contiguous), h_root, leaf tabulations
         uw = pool[:2 * N, 0].cpu().numpy()
         rs = lay["hslot"][self.tree.root]
@@ -321,9 +364,42 @@ class FactorizedSolver:
         if down:
             uc = pool[lay["UC"]:lay["UC"] + nl * P, 0].cpu().numpy().reshape(nl, P)
             st.leaf_solutions = self._leaf_view(uc)
-        else:
-            st.scratch = {"g": g}
         return st
+
+    def _downward_host(self, f, state: SolveState) -> SolveState:
+        """Complete `state` (from upward_pass) in place: u on the root exterior = f, then the
+        downward sweep u[j3] = S u_ext + state.w[j3] and the leaf tabulations from state.g_tab
+        (reference solver.py:293-335, 428-432). Nothing of the upward sweep is re-run: the
+        particular solutions come from the state, as in the reference."""
+        fv = self._dirichlet(f)
+        nl, m, P, N = self._n_leaves, (self.p - 2) ** 2, self.p ** 2, self.plan.n_gauss
+        gt = self._state_loads(state)
+        w = np.asarray(state.w, dtype=np.float64)
+        if w.shape != (N,):
+            raise ValueError(f"state.w has shape {w.shape}, expected ({N},)")
+        with self._lock:
+            prog = self._program(1)
+            lay, pool = self._layout, prog["pool"]
+            pool[lay["G"]:lay["G"] + nl * m, 0].copy_(torch.as_tensor(gt, dtype=torch.float64).reshape(-1))
+            pool[lay["W"]:lay["W"] + N, 0].copy_(torch.from_numpy(w))
+            prog["f_in"][:, 0].copy_(torch.as_tensor(fv, dtype=torch.float64).reshape(-1))
+            self._execute(prog, phase="down")
+            u = pool[lay["U"]:lay["U"] + N, 0].cpu().numpy()
+            uc = pool[lay["UC"]:lay["UC"] + nl * P, 0].cpu().numpy().reshape(nl, P)
+        if isinstance(state.u, np.ndarray) and state.u.shape == (N,) and state.u.flags.writeable:
+            state.u[:] = u
+        else:
+            state.u = u
+        state.leaf_solutions = self._leaf_view(uc)
+        state.scratch = None
+        return state
+
+    def _state_loads(self, state):
+        """(n_leaves, m) table of a state's body-load tabulations (SolveState.g_tab)."""
+        gt = state.g_tab
+        if isinstance(gt, LeafSolutions) and gt._row is getattr(self, "_leaf_rowmap", None):
+            return gt._table
+        return self._leaf_table(gt if len(gt) else None)
 
     def _run_overlapped(self, prog) -> SolveState:
         """Solve with the device->host reads overlapped: the graph replays everything up to the
@@ -365,60 +441,84 @@ class FactorizedSolver:
     def _out_buffers(self, prog, sizes):
         """Host result buffers for one host-API solve, as (torch view, numpy array) pairs.
         Page-locked blocks read 3x faster than pageable memory here, but pinning costs ~ms per MB,
-        so two sets are allocated once per program and handed out again only when no array of an
-        earlier SolveState still refers to them (the returned arrays are views of the ring's numpy
-        arrays, so their reference counts tell); a caller that keeps its states gets fresh
-        pageable arrays instead."""
+        so two sets are allocated once per program and lent out. Each loan wraps the page-locked
+        memory in a fresh _HostLease that is the numpy arrays' base object: every array, view or
+        Mapping of a returned SolveState keeps its lease alive, and the set is lent again only
+        once the lease has been garbage-collected (a weak reference tells). A caller that keeps
+        its states gets fresh pageable arrays instead."""
         ring = prog.setdefault("out_ring", [])
-        for bufs in ring:
-            # free: only the ring's tuple, the loop variable and the getrefcount argument refer
-            # to the array
-            if all(sys.getrefcount(a) <= 3 for _, a in bufs):
-                return bufs
-        if len(ring) < 2:
-            ts = [torch.empty(n, dtype=torch.float64, pin_memory=True) for n in sizes]
-            bufs = [(t, t.numpy()) for t in ts]
-            ring.append(bufs)
-            return bufs
-        return [(torch.from_numpy(a), a) for a in (np.empty(n) for n in sizes)]
+        slot = None
+        for entry in ring:
+            if all(ref is None or ref() is None for ref in entry["leases"]):
+                slot = entry
+                break
+        if slot is None and len(ring) < 2:
+            slot = {"pinned": [torch.empty(n, dtype=torch.float64, pin_memory=True) for n in sizes],
+                    "leases": [None] * len(sizes)}
+            ring.append(slot)
+        if slot is None:
+            return [(torch.from_numpy(a), a) for a in (np.empty(n) for n in sizes)]
+        out = []
+        for i, t in enumerate(slot["pinned"]):
+            lease = _HostLease(t)
+            slot["leases"][i] = weakref.ref(lease)
+            out.append((t, np.asarray(lease)))
+        return out
 
-    def solve_device(self, f: torch.Tensor, g: torch.Tensor) -> dict:
+    def solve_device(self, f: torch.Tensor, g: torch.Tensor, out: dict | None = None) -> dict:
         """Multi-RHS solve with device-resident inputs and outputs (no host round trip).
 
         f: (|root ext|, nrhs) Dirichlet data in plan.node[root].ext order;
         g: (n_leaves * m, nrhs) interior loads in leaf-row order (i_ci order within a leaf).
-        Returns views into the solver's vector pool (valid until the next solve with the
-        same nrhs): u, w (N_gauss, nrhs), uc (n_leaves, P, nrhs), g.
+        Returns u, w (N_gauss, nrhs), uc (n_leaves, P, nrhs) and g. Without `out` these are views
+        into the solver's vector pool, valid until the next solve with the same nrhs (the
+        zero-copy form the time steppers use). With `out` (a dict holding any of "u", "w", "uc"
+        as caller-owned device tensors of those shapes) the results are copied there on the
+        current stream before the call returns, so the caller's tensors survive later solves.
         """
         nrhs = g.shape[-1]
-        prog = self._program(nrhs)
-        lay, pool, N = self._layout, prog["pool"], self.plan.n_gauss
-        nl, P, m = self._n_leaves, self.p ** 2, (self.p - 2) ** 2
-        pool[lay["G"]:lay["G"] + nl * m].copy_(g.reshape(-1, nrhs))
-        prog["f_in"].copy_(f.reshape(-1, nrhs))
-        self._execute(prog, down=True)
-        return {"u": pool[lay["U"]:lay["U"] + N], "w": pool[lay["W"]:lay["W"] + N],
-                "uc": pool[lay["UC"]:lay["UC"] + nl * P].view(nl, P, nrhs),
-                "g": pool[lay["G"]:lay["G"] + nl * m]}
+        with self._lock:
+            prog = self._program(nrhs)
+            lay, pool, N = self._layout, prog["pool"], self.plan.n_gauss
+            nl, P, m = self._n_leaves, self.p ** 2, (self.p - 2) ** 2
+            pool[lay["G"]:lay["G"] + nl * m].copy_(g.reshape(-1, nrhs))
+            prog["f_in"].copy_(f.reshape(-1, nrhs))
+            self._execute(prog, phase="full")
+            res = {"u": pool[lay["U"]:lay["U"] + N], "w": pool[lay["W"]:lay["W"] + N],
+                   "uc": pool[lay["UC"]:lay["UC"] + nl * P].view(nl, P, nrhs),
+                   "g": pool[lay["G"]:lay["G"] + nl * m]}
+            if out:
+                for k, t in out.items():
+                    t.copy_(res[k].reshape(t.shape))
+                    res[k] = t
+            return res
 
     # -- sweep program ----------------------------------------------------------------------
     use_graphs = True
 
-    def _steps(self, prog, down=True, leaves_down=True):
-        """Enqueue one solve on the current stream: zero u/w, upward sweep, f, downward sweep
-        (leaves_down=False: everything but the final leaf step, see _solve_host)."""
+    def _steps(self, prog, phase="full", leaves_down=True):
+        """Enqueue one solve on the current stream (leaves_down=False: everything but the final
+        leaf step, see _run_overlapped). phase "full": upward sweep, f, downward sweep; "up": the
+        upward pass alone (upward_pass); "down": the downward pass alone from the w and g rows
+        already in the pool (downward_pass)."""
         lib = _ext.load()
         pool = prog["pool"]
         N = self.plan.n_gauss
         s = _stream_ptr()
-        if not down:
+        if phase == "down":
+            # u[j3] = S u_ext + w[j3] from the state's w (reference solver.py:329-335)
+            _ext.check(lib.hps_sweep_gemv(prog["copy_f"], s), "Dirichlet copy")
+            for step in prog["down_w"]:
+                _ext.check(lib.hps_sweep_gemv(step, s), "downward sweep")
+            return
+        if phase == "up":
             # upward pass only: u must read zero (reference solver.py:418-425). A full solve
             # needs no clearing: every u row is written (root exterior by the Dirichlet copy,
             # each J3 set by its parent) and w rows outside the J3 sets are never written
             pool[:2 * N].zero_()
         for step in prog["up"]:
             _ext.check(lib.hps_sweep_gemv(step, s), "upward sweep")
-        if not down:
+        if phase == "up":
             for step in prog["wonly"]:
                 _ext.check(lib.hps_sweep_gemv(step, s), "upward sweep (w3)")
             return
@@ -450,18 +550,22 @@ class FactorizedSolver:
             prog[key] = g
         return g
 
-    def _execute(self, prog, down=True):
+    def _execute(self, prog, phase="full"):
         if self.mode == "econ":
             lib = _ext.load()
             s = _stream_ptr()
             fresh = [_leaf_build_call(grp, self.p, self.q, lib, s) for grp in self.leaf_groups]
             for pas, i, (kind, gi) in prog["patches"]:
                 prog[pas][i].A.base = (fresh[gi][0] if kind == "fs" else fresh[gi][1]).data_ptr()
-            self._steps(prog, down)
+            # the sweep kernels stage operator rows BEFORE their programmatic-launch wait
+            # (operators are static while a program runs); the freshly rebuilt leaf operators
+            # are published by one ordinary (non-PDL) launch between the build and the sweep
+            prog.setdefault("fence", torch.zeros(1, dtype=torch.float64, device=self.device)).zero_()
+            self._steps(prog, phase)
             del fresh  # stream-ordered: the allocator reuses the blocks only for later work
             return
-        if not (down and self.use_graphs):
-            self._steps(prog, down)
+        if not (phase == "full" and self.use_graphs):
+            self._steps(prog, phase)
             return
         self._graph(prog, "graph").replay()
 
@@ -550,6 +654,25 @@ class FactorizedSolver:
             j3 = np.stack([plan.node[n].j3 for n in grp.ids])
             down.append(gemv(len(grp.ids), m3, m3 + e, _ext.mat(grp.xs, m3 * (m3 + e), m3 + e), xi,
                              lay["U"] + j3, x2idx=x2, mode2=3, R2=m3, K2=m3, o2idx=ow))
+        # downward pass from a stored w (downward_pass): u[j3] = S u_ext + w[j3] with S the last
+        # e (e_c) columns of [X | S] (solver.py:329-335)
+        down_w = []
+        for grp in sorted(self.parent_groups, key=lambda g_: g_.depth):
+            m3, e = grp.m3, grp.e
+            if grp.wrap is not None:
+                nid = grp.ids[0]
+                en = plan.node[nid]
+                ec = grp.wrap["ec"]
+                ext = lay["U"] + en.ext
+                down_w.append(gemv(1, e, ec, _ext.mat(grp.wrap["pu_dev"], 0, ec), ext[None],
+                                   (lay["U"] + en.wrap.fine)[None]))
+                down_w.append(gemv(1, m3, ec, _ext.mat(grp.wrap["xsw"], 0, m3 + ec, off=m3), ext[None],
+                                   (lay["U"] + en.j3)[None], aidx=(lay["W"] + en.j3)[None]))
+                continue
+            ext = np.stack([lay["U"] + plan.node[n].ext_mergeorder for n in grp.ids])
+            j3 = np.stack([plan.node[n].j3 for n in grp.ids])
+            down_w.append(gemv(len(grp.ids), m3, e, _ext.mat(grp.xs, m3 * (m3 + e), m3 + e, off=m3), ext,
+                               lay["U"] + j3, aidx=lay["W"] + j3))
         # leaves: u_c[i_ci] = [F | S] [g; u_ext], fused tail stage u_c[i_ce] = L u_ext  (solver.py:325-327)
         for gi, grp in enumerate(self.leaf_groups):
             L = len(grp.ids)
@@ -562,12 +685,14 @@ class FactorizedSolver:
                              base + grp.sc.i_ci[None, :], mode2=1, R2=c, K2=b,
                              A2=_ext.mat(grp.consts["lift"], 0, b), o2idx=base + grp.sc.i_ce[None, :]))
             down[-1]["patch"] = ("fs", self.leaf_groups.index(grp))
+            down_w.append(dict(down[-1]))
         # split-K for steps with long rows and too few CTAs (top of the tree): partial products
         # into scratch pool rows, then a deterministic reduction step (A = ones)
         scratch = [lay["rows"]]
 
         def split(spec):
-            if spec["mode2"] not in (0, 3) or spec["K"] < 512:
+            if spec["mode2"] not in (0, 3) or spec["K"] < 512 or "patch" in spec:
+                # (economy-mode leaf steps take their operator base per solve: never split)
                 return [spec]
             K = spec["K"]
             # the single-launch sweep program stages each step's x in 48 KB of shared memory
@@ -636,6 +761,7 @@ class FactorizedSolver:
         up = [s2 for s1 in up for s2 in split(s1)]
         down = [s2 for s1 in down for s2 in split(s1)]
         wonly = [s2 for s1 in wonly for s2 in split(s1)]
+        down_w = [s2 for s1 in down_w for s2 in split(s1)]
         # Dirichlet data: rows F of the pool, copied onto the root exterior by a 1x1 "gemv" step
         root_ext = plan.node[tree.root].ext
         f_rows = scratch[0]
@@ -669,7 +795,7 @@ class FactorizedSolver:
                                   xi.data_ptr(), _ext.ptr(x2), _ext.ptr(ai), oi.data_ptr(), spec["mode2"],
                                   spec["R2"], spec["K2"], A2, _ext.ptr(a2), _ext.ptr(o2))
 
-        patches = [(k, i, s_["patch"]) for k, lst in (("up", up), ("down", down))
+        patches = [(k, i, s_["patch"]) for k, lst in (("up", up), ("down", down), ("down_w", down_w))
                    for i, s_ in enumerate(lst) if "patch" in s_]
         ng = len(self.leaf_groups)
         up = [build(s_) for s_ in up]
@@ -693,8 +819,10 @@ class FactorizedSolver:
                     cb.o2idx = gb.o2idx + 4 * i0 * gb.R2
                 leaf_chunks.append((cb, grp.first_row + i0, grp.first_row + i1))
         wonly = [build(s_) for s_ in wonly]
+        down_w = [build(s_) for s_ in down_w]
         f_in = pool[f_rows:f_rows + root_ext.size]
-        prog = {"pool": pool, "up": up, "down": down, "wonly": wonly, "keep": keep, "f_in": f_in, "copy_f": copy_f,
+        prog = {"pool": pool, "up": up, "down": down, "wonly": wonly, "down_w": down_w, "keep": keep,
+                "f_in": f_in, "copy_f": copy_f,
                 "leaf_chunks": leaf_chunks,
                 "graph": None, "patches": patches}
         self._sweeps[nrhs] = prog
@@ -909,7 +1037,7 @@ def _build_device(solver: FactorizedSolver, order, profile=False):
             ta_ptr = _ptr_array([t.data_ptr() + 8 * off for t, off, _ in ta], dev)
             tb_ptr = _ptr_array([t.data_ptr() + 8 * off for t, off, _ in tb], dev)
             idx = _upload(rows_idx, dev)
-            grp.xs = torch.empty((npar, m3, m3 + e), dtype=torch.float64, device=dev)
+            grp.xs = _op_empty((npar, m3, m3 + e), dev)
             grp.tei = torch.empty((npar, e, m3), dtype=torch.float64, device=dev)
             grp.tnew = torch.empty((npar, e, e), dtype=torch.float64, device=dev)
             grp.dnorm = torch.empty(npar, dtype=torch.float64, device=dev)
@@ -967,8 +1095,8 @@ def _leaf_build_call(grp, p, q, lib, s):
     dev = grp.coef.device
     L = len(grp.ids)
     m, b = (p - 2) ** 2, 4 * q
-    fs = torch.empty((L, m, m + b), dtype=torch.float64, device=dev)
-    h = torch.empty((L, b, m), dtype=torch.float64, device=dev)
+    fs = _op_empty((L, m, m + b), dev)
+    h = _op_empty((L, b, m), dev)
     t = torch.empty((L, b, b), dtype=torch.float64, device=dev)
     ws = torch.empty(int(lib.hps_leaf_workspace_bytes(L, p, q)), dtype=torch.uint8, device=dev)
     if grp.perm is None:
@@ -997,10 +1125,10 @@ def _apply_wrap(solver, grp, en, lib, s):
     qd[:, perm] = pd
     qu = np.zeros((e, ec))
     qu[perm, :] = pu
-    qd_t, qu_t, pu_t = _f64(qd, dev), _f64(qu, dev), _f64(pu, dev)
+    qd_t, qu_t, pu_t = _op_f64(qd, dev), _f64(qu, dev), _op_f64(pu, dev)
     tmp = torch.empty((ec, e), dtype=torch.float64, device=dev)
     tw = torch.empty((ec, ec), dtype=torch.float64, device=dev)
-    xsw = torch.empty((m3, m3 + ec), dtype=torch.float64, device=dev)
+    xsw = _op_empty((m3, m3 + ec), dev)
     xsw[:, :m3].copy_(grp.xs[0, :, :m3])
 
     def gemm(M, N, K, A, B, C):
@@ -1076,12 +1204,10 @@ def upward_pass(solver: FactorizedSolver, g=None) -> SolveState:
 
 
 def downward_pass(solver: FactorizedSolver, f, state: SolveState) -> SolveState:
-    """Complete a state from upward_pass with Dirichlet data f (reference solver.py:428-432).
-    The device program re-runs the (deterministic) upward sweep with the same load."""
-    g = state.scratch.get("g") if state.scratch else None
-    full = solver._solve_host(f, g, down=True)
-    full.scratch = None
-    return full
+    """Complete a state produced by upward_pass with the Dirichlet sweep, in place (reference
+    solver.py:428-432): the state's own w and g_tab feed the downward sweep; the same object is
+    returned with u and leaf_solutions filled and scratch cleared."""
+    return solver._downward_host(f, state)
 
 
 def solve(solver: FactorizedSolver, f=None, g=None) -> SolveState:

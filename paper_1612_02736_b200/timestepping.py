@@ -185,7 +185,7 @@ class DeviceStepper:
         base = self.pool.data_ptr()
         self.ctx.apply_ptr(base + 8 * n * lay["UC"], base + 8 * n * lay["G"], n, self.alpha, self.beta)
         self.prog["f_in"].copy_(f.reshape(-1, self.nrhs))
-        self.solver._execute(self.prog, down=True)
+        self.solver._execute(self.prog)
 
 
 def _leaf_points(solver: FactorizedSolver) -> np.ndarray:

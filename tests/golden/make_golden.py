@@ -214,6 +214,153 @@ def solve_fixtures():
     save("cfg5_n4.npz", **a)
 
 
+PROJ_SEED = 99
+
+
+def proj_weights(n):
+    """Fixed seeded projection vector (standard normal) of length n, shared with the tests."""
+    return np.random.default_rng([PROJ_SEED, n]).standard_normal(n)
+
+
+def cover_all(st, q):
+    """Fingerprint that covers EVERY leaf and every Gauss segment: per leaf, the max-norm and a
+    seeded random projection w . u_c of its tabulation; per edge segment (q nodes, global ids
+    seg*q + k), a projection of its q values. A wrong value anywhere moves one of them."""
+    ids = sorted(st.leaf_solutions)
+    tabs = np.stack([st.leaf_solutions[i] for i in ids])
+    u = np.asarray(st.u)
+    return {"all_leaf_ids": np.array(ids), "all_leaf_absmax": np.abs(tabs).max(axis=1),
+            "all_leaf_proj": tabs @ proj_weights(tabs.shape[1]),
+            "seg_proj": u.reshape(-1, q) @ proj_weights(q)}
+
+
+def be_loads_ref(tabs, tree, p, q, dt):
+    g = {}
+    for lf in tree.leaves():
+        geo = leaf_geometry(p, q, lf.bounds.width, lf.bounds.height)
+        g[lf.id] = np.asarray(tabs[lf.id])[geo.stencil0.i_ci] / dt
+    return g
+
+
+def initial_tabs(tree, p, q, seed):
+    u0 = problems.config5_initial(seed=seed)
+    tabs = {}
+    for lf in tree.leaves():
+        geo = leaf_geometry(p, q, lf.bounds.width, lf.bounds.height)
+        tabs[lf.id] = u0(stencil_for(lf.bounds, geo).cheb2d)
+    return tabs
+
+
+def cfg5_trajectory_fixture(nrhs=16, steps=3):
+    """Config 5 at its real shape, run by the reference: 128x128 leaves, p=16, dt=1e-3, the 16
+    seeded initial fields (seeds 0..15), `steps` backward-Euler steps each through the reference's
+    own FactorizedSolver.solve loop (solver.py:337-354; g = u_c[i_ci]/dt, f = sin(2 pi t) x1 (1-x2)).
+    Per step: every leaf of every RHS enters an RHS-mixed projection sum_r c_r (w . u_c^r); per
+    RHS, u on 500 seeded Gauss nodes and max-norms. At the last step: the RHS-mixed projection of
+    every Gauss segment and four complete leaf tabulations per RHS."""
+    import time
+    dt, p, q = 1e-3, 16, 15
+    tree = build_uniform_tree(UNIT, 128)
+    t0 = time.perf_counter()
+    solver = build_stage(tree, problems.config5_spec(dt), p, q)
+    print(f"cfg5 build {time.perf_counter() - t0:.1f} s")
+    rng = np.random.default_rng(515)
+    ids = sorted(lf.id for lf in tree.leaves())
+    upick = np.sort(rng.choice(solver.plan.n_gauss, size=500, replace=False))
+    lpick = np.sort(rng.choice(len(ids), size=4, replace=False))
+    cmix = np.random.default_rng([PROJ_SEED, 16, 1]).standard_normal(nrhs)
+    wP = proj_weights(p * p)
+    out = {"u_idx": upick, "leaf_pick": np.array([ids[i] for i in lpick]), "leaf_ids": np.array(ids),
+           "mix_proj": np.zeros((steps, len(ids))), "u_vals": np.zeros((steps, nrhs, upick.size)),
+           "u_max": np.zeros((steps, nrhs)), "leaf_max": np.zeros((steps, nrhs)),
+           "mix_seg": np.zeros(solver.plan.n_gauss // q),
+           "leaf_sol": np.zeros((nrhs, lpick.size, p * p)), "steps": np.array([steps]),
+           "nrhs": np.array([nrhs])}
+    for r in range(nrhs):
+        t1 = time.perf_counter()
+        tabs = initial_tabs(tree, p, q, r)
+        for k in range(1, steps + 1):
+            t = k * dt
+            st = solver.solve(f=lambda pts, _t=t: problems.config5_dirichlet(pts, _t),
+                              g=be_loads_ref(tabs, tree, p, q, dt))
+            tabs = st.leaf_solutions
+            T = np.stack([tabs[i] for i in ids])
+            out["mix_proj"][k - 1] += cmix[r] * (T @ wP)
+            out["u_vals"][k - 1, r] = st.u[upick]
+            out["u_max"][k - 1, r] = np.abs(st.u).max()
+            out["leaf_max"][k - 1, r] = np.abs(T).max()
+        out["mix_seg"] += cmix[r] * (st.u.reshape(-1, q) @ proj_weights(q))
+        out["leaf_sol"][r] = T[lpick]
+        print(f"  rhs {r}: {time.perf_counter() - t1:.1f} s")
+    save("full_cfg5_traj.npz", **out)
+
+
+def cfg5_drift_fixture(n=16, steps=50):
+    """Long single-RHS backward-Euler trajectory (seed 0) at n x n leaves, for drift: fingerprints
+    after steps 1, 10 and `steps`, plus the complete u and all leaf tabulations at the end."""
+    dt, p, q = 1e-3, 16, 15
+    tree = build_uniform_tree(UNIT, n)
+    solver = build_stage(tree, problems.config5_spec(dt), p, q)
+    tabs = initial_tabs(tree, p, q, 0)
+    ids = sorted(lf.id for lf in tree.leaves())
+    keep = (1, 10, steps)
+    out = {"leaf_ids": np.array(ids), "keep": np.array(keep), "n": np.array([n])}
+    for k in range(1, steps + 1):
+        t = k * dt
+        st = solver.solve(f=lambda pts, _t=t: problems.config5_dirichlet(pts, _t),
+                          g=be_loads_ref(tabs, tree, p, q, dt))
+        tabs = st.leaf_solutions
+        if k in keep:
+            for key, v in cover_all(st, q).items():
+                out[f"s{k}_{key}"] = v
+            out[f"s{k}_u_max"] = np.array([np.abs(st.u).max()])
+    out["u_final"] = st.u
+    out["leaf_sol_final"] = np.stack([tabs[i] for i in ids])
+    save(f"cfg5_drift_n{n}.npz", **out)
+
+
+def resonance_fixture():
+    """A Helmholtz wavenumber at an interface resonance of the first merge, found with the
+    reference's own leaf operators: on a 2x2 mesh (p=12, q=11) box 2 = [0.5,1]x[0,1] has the
+    Dirichlet eigenvalue 5 pi^2, so kappa ~ sqrt(5) pi makes Delta = T33_a - T33_b singular. A
+    secant iteration drives the eigenvalue of Delta nearest zero to round-off, then the
+    reference's build_stage is run to record the box and message it raises
+    (MergeSingularError, solver.py:108-119)."""
+    from specdtn.solver import MergeSingularError
+    tree = build_uniform_tree(UNIT, 2)
+    p, q = 12, 11
+    plan = enumerate_gauss_nodes(tree, q)
+    par = [n for n in range(len(tree.nodes) - 1, -1, -1) if not tree.nodes[n].is_leaf][0]
+    ca, cb = tree.nodes[par].children
+    en = plan.node[par]
+
+    def lam(k):
+        spec = catalog("helmholtz", kappa=k)
+        ta = build_leaf_operators(tree.nodes[ca], spec, p, q).T
+        tb = build_leaf_operators(tree.nodes[cb], spec, p, q).T
+        w = np.linalg.eigvals(ta[np.ix_(en.pos3_a, en.pos3_a)] - tb[np.ix_(en.pos3_b, en.pos3_b)])
+        return w[np.argmin(np.abs(w))].real
+
+    a, b = np.sqrt(5.0) * np.pi * 0.9999, np.sqrt(5.0) * np.pi
+    fa, fb = lam(a), lam(b)
+    for _ in range(30):
+        if fb == fa:
+            break
+        a, fa, b = b, fb, b - fb * (b - a) / (fb - fa)
+        fb = lam(b)
+        if abs(fb) < 1e-14:
+            break
+    try:
+        build_stage(tree, catalog("helmholtz", kappa=b), p, q)
+        raise SystemExit("reference did not raise at the resonant kappa")
+    except MergeSingularError as exc:
+        msg = str(exc)
+    box = int(msg.split("box ")[1].split()[0])
+    print("resonance", repr(b), msg)
+    save("resonance.npz", kappa=np.array([b]), p=np.array([p]), q=np.array([q]), n=np.array([2]),
+         box=np.array([box]), lam=np.array([fb]))
+
+
 def fullsize_fixture():
     """BASELINE configs 2-5 at their full sizes, run by the reference itself. The full solutions
     are too large to commit, so the fixture keeps a fingerprint: norms of u, u on 2000 seeded
@@ -233,6 +380,7 @@ def fullsize_fixture():
                "u_l2": np.array([np.linalg.norm(st.u)]), "leaf_ids": np.array([ids[i] for i in pick]),
                "leaf_sol": np.stack([st.leaf_solutions[ids[i]] for i in pick]),
                "leaf_max": np.array([max(np.abs(v).max() for v in st.leaf_solutions.values())])}
+        out.update(cover_all(st, q))
         if spec.u_exact is not None:
             out["linf_error"] = np.array([linf_error(st, ReferenceSolution.analytic(spec.u_exact))])
         out.update(extra or {})
@@ -272,6 +420,13 @@ if __name__ == "__main__":
         raise SystemExit
     if "--only-plans" in _sys.argv:
         plan_fixture()
+        raise SystemExit
+    if "--only-resonance" in _sys.argv:
+        resonance_fixture()
+        raise SystemExit
+    if "--only-traj" in _sys.argv:
+        cfg5_drift_fixture()
+        cfg5_trajectory_fixture()
         raise SystemExit
     if "--only-full" in _sys.argv:
         fullsize_fixture()

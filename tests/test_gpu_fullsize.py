@@ -15,6 +15,10 @@ pytestmark = pytest.mark.gpu
 UNIT = (0.0, 1.0, 0.0, 1.0)
 
 
+def proj_weights(n):
+    return np.random.default_rng([99, n]).standard_normal(n)  # make_golden.py PROJ_SEED
+
+
 def _check(fx, st, tol):
     u = np.asarray(st.u)
     assert abs(np.abs(u).max() - fx["u_max"][0]) <= tol * fx["u_max"][0]
@@ -23,6 +27,16 @@ def _check(fx, st, tol):
     assert np.abs(u[fx["u_idx"]] - fx["u_vals"]).max() <= tol * fx["u_max"][0]
     sol = np.stack([st.leaf_solutions[int(i)] for i in fx["leaf_ids"]])
     assert np.abs(sol - fx["leaf_sol"]).max() <= tol * fx["leaf_max"][0]
+    # every leaf and every Gauss segment: per-leaf max-norms and seeded projections
+    # (|w . d| <= ||w||_1 max|d|), so a wrong value on any leaf or edge fails
+    scale = fx["leaf_max"][0]
+    tabs = np.stack([st.leaf_solutions[int(i)] for i in fx["all_leaf_ids"]])
+    assert np.abs(np.abs(tabs).max(axis=1) - fx["all_leaf_absmax"]).max() <= tol * scale
+    wP = proj_weights(tabs.shape[1])
+    assert np.abs(tabs @ wP - fx["all_leaf_proj"]).max() <= tol * scale * np.abs(wP).sum()
+    q = u.size // fx["seg_proj"].size
+    wq = proj_weights(q)
+    assert np.abs(u.reshape(-1, q) @ wq - fx["seg_proj"]).max() <= tol * max(scale, fx["u_max"][0]) * np.abs(wq).sum()
 
 
 def test_config2_full_size():

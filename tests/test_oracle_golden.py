@@ -86,3 +86,22 @@ def test_config5_small_backward_euler():
             tabs = st["leaf_solutions"]
         sol = np.stack([tabs[i] for i in sorted(tabs)])
         assert rel_maxdiff(sol, fx[f"rhs{r}_leaf_sol"]) < 1e-11
+
+
+def test_be_drift_50_steps():
+    """The oracle reproduces the reference's 50-step backward-Euler trajectory (16x16 leaves,
+    seed 0; tests/golden/cfg5_drift_n16.npz) — pins the BE harness the GPU drift test checks."""
+    fx = golden("cfg5_drift_n16.npz")
+    dt, p, q = 1e-3, 16, 15
+    tree = build_uniform_tree(UNIT, int(fx["n"][0]))
+    plan = enumerate_gauss_nodes(tree, q)
+    ops = orc.build(tree, problems.config5_spec(dt), p, q, plan)
+    u0 = problems.config5_initial(0)
+    tabs = {lf.id: u0(orc.leaf_points(lf.bounds, p, q)) for lf in tree.leaves()}
+    bpts = plan.coords[plan.node[tree.root].ext]
+    for k in range(1, int(fx["keep"][-1]) + 1):
+        st = orc.solve(ops, problems.config5_dirichlet(bpts, k * dt), orc.be_loads(tabs, tree, p, q, dt))
+        tabs = st["leaf_solutions"]
+    ids = fx["leaf_ids"]
+    assert rel_maxdiff(np.stack([tabs[int(i)] for i in ids]), fx["leaf_sol_final"]) < 1e-11
+    assert rel_maxdiff(st["u"], fx["u_final"]) < 1e-11
