@@ -271,8 +271,9 @@ class FactorizedSolver:
             rm = self._leaf_rowmap = {int(n): r for r, n in enumerate(self._leaf_ids)}
         return LeafSolutions(None, None, table, rowmap=rm)
 
-    def _leaf_table(self, g):
-        """(n_leaves, m) interior body-load table in leaf-row order (solver.py:241-253)."""
+    def _leaf_table(self, g, out=None):
+        """(n_leaves, m) interior body-load table in leaf-row order (solver.py:241-253). With
+        `out` (an (n_leaves, m) float64 array) a mapping input is gathered straight into it."""
         if g is None:
             g = self.spec.body_load
         nl = self._n_leaves
@@ -294,19 +295,26 @@ class FactorizedSolver:
         if isinstance(g, LeafSolutions) and g._row is getattr(self, "_leaf_rowmap", None):
             tab = np.asarray(g._table, dtype=float)  # a state's own g_tab: already leaf-row order
             if tab.shape == (nl, m):
-                return tab
-        # mapping {leaf id: (m,)} (reference solver.py:246-252): one gather in leaf-row order
+                if out is None:
+                    return tab
+                out[:] = tab
+                return out
+        # mapping {leaf id: (m,)} (reference solver.py:246-252): one gather in leaf-row order,
+        # concatenated in C into the destination (no per-leaf Python work beyond the lookups)
         vals = [g[nid] for nid in self._leaf_ids]
+        dst = out if out is not None else np.empty((nl, m))
         try:
-            out = np.asarray(vals, dtype=float)
-        except ValueError:
-            out = None
-        if out is None or out.shape != (nl, m):
-            for nid, v in zip(self._leaf_ids, vals):
-                shp = np.shape(v)
-                if shp != (m,):
-                    raise ValueError(f"leaf {nid} load has shape {shp}, expected ({m},)")
-        return out
+            if set(map(len, vals)) == {m}:
+                np.concatenate(vals, out=dst.reshape(-1))
+                return dst
+        except (TypeError, ValueError):
+            pass
+        for nid, v in zip(self._leaf_ids, vals):
+            shp = np.shape(v)
+            if shp != (m,):
+                raise ValueError(f"leaf {nid} load has shape {shp}, expected ({m},)")
+        dst[:] = np.asarray(vals, dtype=float)
+        return dst
 
     def _interior_points(self, grp):
         sc = grp.sc
@@ -336,22 +344,47 @@ class FactorizedSolver:
 
     def _solve_host(self, f, g, down=True) -> SolveState:
         fv = self._dirichlet(f) if down else None
-        gt = self._leaf_table(g)
         with self._lock:
-            return self._solve_host_locked(fv, gt, g, down)
+            return self._solve_host_locked(fv, g, down)
 
-    def _solve_host_locked(self, fv, gt, g, down) -> SolveState:
+    def _upload_loads(self, prog, g):
+        """Body load -> the pool's G rows. Host inputs go through one page-locked staging buffer
+        per program (a mapping is concatenated straight into it) and one asynchronous copy.
+        Returns the SolveState.g_tab: the caller's mapping itself (as the reference keeps the
+        caller's g_ci arrays, solver.py:279), else a leaf-id view of the table."""
+        lay, pool = self._layout, prog["pool"]
+        nl, m = self._n_leaves, (self.p - 2) ** 2
+        g_rows = pool[lay["G"]:lay["G"] + nl * m, 0]
+        if g is None:
+            g = self.spec.body_load
+        if isinstance(g, torch.Tensor):
+            if tuple(g.shape) != (nl, m):
+                raise ValueError(f"load table has shape {tuple(g.shape)}, expected ({nl}, {m})")
+            g_rows.copy_(g.reshape(-1))
+            return self._leaf_view(g.detach().cpu().numpy())
+        stage = prog.get("g_stage")
+        if stage is None:
+            stage = prog["g_stage"] = torch.empty(nl * m, dtype=torch.float64, pin_memory=True)
+        if isinstance(g, Mapping):
+            self._leaf_table(g, out=stage.numpy().reshape(nl, m))
+            tab = g
+        else:
+            table = self._leaf_table(g)
+            stage.numpy().reshape(nl, m)[:] = table
+            tab = self._leaf_view(np.asarray(table))
+        g_rows.copy_(stage, non_blocking=True)
+        return tab
+
+    def _solve_host_locked(self, fv, g, down) -> SolveState:
         prog = self._program(1)
         lay, pool = self._layout, prog["pool"]
         N, P, nl = self.plan.n_gauss, self.p ** 2, self._n_leaves
-        g_rows = pool[lay["G"]:lay["G"] + nl * (self.p - 2) ** 2, 0]
-        g_rows.copy_(torch.as_tensor(gt, dtype=torch.float64).reshape(-1), non_blocking=False)
+        gtab = self._upload_loads(prog, g)
         if down:
             prog["f_in"][:, 0].copy_(torch.as_tensor(fv, dtype=torch.float64).reshape(-1))
         if down and self.use_graphs and self.mode != "econ":
             st = self._run_overlapped(prog)
-            gtab = gt.detach().cpu().numpy() if isinstance(gt, torch.Tensor) else np.asarray(gt)
-            st.g_tab = self._leaf_view(gtab)
+            st.g_tab = gtab
             return st
         self._execute(prog, phase="full" if down else "up")
         # D2H of the result regions only: U|W (contiguous), h_root, leaf tabulations
@@ -359,8 +392,7 @@ class FactorizedSolver:
         rs = lay["hslot"][self.tree.root]
         st = SolveState(u=uw[:N], w=uw[N:], tree=self.tree, p=self.p, q=self.q,
                         h_root=pool[rs:rs + lay["hsize"][self.tree.root], 0].cpu().numpy())
-        gtab = gt.detach().cpu().numpy() if isinstance(gt, torch.Tensor) else np.asarray(gt)
-        st.g_tab = self._leaf_view(gtab)
+        st.g_tab = gtab
         if down:
             uc = pool[lay["UC"]:lay["UC"] + nl * P, 0].cpu().numpy().reshape(nl, P)
             st.leaf_solutions = self._leaf_view(uc)

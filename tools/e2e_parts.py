@@ -13,6 +13,7 @@ from paper_1612_02736_b200.geometry import enumerate_gauss_nodes
 tree, spec, p, q, desc = bench.make_config(int(sys.argv[1]) if len(sys.argv) > 1 else 2, 0)
 solver = build_stage(tree, spec, p, q, plan=enumerate_gauss_nodes(tree, q))
 g = solver._leaf_table(None)
+gd = {int(n): g[r] for r, n in enumerate(solver._leaf_ids)}
 f = solver._dirichlet(None)
 for _ in range(3):
     solver.solve(f=f, g=g)
@@ -37,6 +38,9 @@ gdev = pool[lay["G"]:lay["G"] + nl * m, 0]
 gt = torch.as_tensor(g).reshape(-1)
 gpin = gt.pin_memory()
 print("full solve (host API)     %.3f ms" % tm(lambda: solver.solve(f=f, g=g)))
+print("full solve (dict g)       %.3f ms" % tm(lambda: solver.solve(f=f, g=gd)))
+stage = np.empty((nl, m))
+print("dict -> table (concat)    %.3f ms" % tm(lambda: solver._leaf_table(gd, out=stage)))
 print("H2D g pageable            %.3f ms  (%.1f MB)" % (tm(lambda: gdev.copy_(gt)), g.nbytes / 1e6))
 print("H2D g pinned non_blocking %.3f ms" % tm(lambda: gdev.copy_(gpin, non_blocking=True)))
 print("graph replay              %.3f ms" % tm(lambda: solver._execute(prog)))
@@ -56,6 +60,6 @@ import pstats
 pr = cProfile.Profile()
 pr.enable()
 for _ in range(20):
-    solver.solve(f=f, g=g)
+    solver.solve(f=f, g=gd)
 pr.disable()
 pstats.Stats(pr).sort_stats("tottime").print_stats(18)
