@@ -124,6 +124,9 @@ typedef struct {
   int* status;
   int* perm;            /* nullable: X left in pivot column order, perm (npar x m3) written */
   void* workspace;      /* hps_merge_workspace_bytes */
+  double* delta;        /* nullable: Delta = T^a_33 - T^b_33 (npar x m3 x m3) copied out before
+                           the elimination, for the reference's (lu, piv) archive sections
+                           (reference archive.py:55-57) */
 } hps_merge_batch;
 long long hps_merge_workspace_bytes(int npar, int m3, int e);
 int hps_merge_build(const hps_merge_batch* b, void* stream);

@@ -36,7 +36,7 @@ class MergeBatch(C.Structure):
                 ("idx", C.c_void_p), ("idx_stride", C.c_longlong), ("xs", C.c_void_p),
                 ("tei", C.c_void_p), ("tnew", C.c_void_p), ("dnorm", C.c_void_p),
                 ("xnorm", C.c_void_p), ("status", C.c_void_p), ("perm", C.c_void_p),
-                ("workspace", C.c_void_p)]
+                ("workspace", C.c_void_p), ("delta", C.c_void_p)]
 
 
 class GemvBatch(C.Structure):

@@ -175,6 +175,10 @@ int hps_merge_build(const hps_merge_batch* Mb, void* stream) {
   a.Tnew = dense(Mb->tnew, (long long)e * e, e);
   int rc = launch_merge_gather(a, s);
   if (rc) return rc;
+  if (Mb->delta &&
+      cudaMemcpy2DAsync(Mb->delta, sizeof(double) * m3, Mb->xs, sizeof(double) * (m3 + e), sizeof(double) * m3,
+                        (size_t)np * m3, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return HPS_ECUDA;
 
   if ((rc = gj_invert(np, m3, m3 + e, dense(Mb->xs, sxs, m3 + e), piv, (double*)gjw, Mb->dnorm, Mb->xnorm,
                       Mb->status, s, Mb->perm)))

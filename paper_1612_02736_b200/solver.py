@@ -99,6 +99,110 @@ def _ptr_array(ptrs, dev):
     return _upload(np.ascontiguousarray(ptrs, dtype=np.int64), dev)
 
 
+@dataclass
+class LeafOperators:
+    """Reference leaf.py:124-135 layout: S (P x 4q), T, F (P x m), H (4q x m), rcond."""
+
+    S: np.ndarray
+    T: np.ndarray | None
+    F: np.ndarray
+    H: np.ndarray
+    rcond: float = float("nan")
+
+    def retained_floats(self) -> int:
+        return self.S.size + self.F.size + self.H.size
+
+
+@dataclass
+class WrapOperators:
+    """Reference solver.py:62-74: interpolation of a refined parent's fine exterior."""
+
+    p_up: np.ndarray
+    p_down: np.ndarray
+    perm: np.ndarray
+    fine: np.ndarray
+
+
+@dataclass
+class ParentOperators:
+    """Reference solver.py:77-105: (lu, piv) of Delta, S (m3 x e), T_ei (e x m3)."""
+
+    lu_piv: tuple
+    s_gi_ge: np.ndarray
+    t_ei: np.ndarray
+    t_ge_ge: np.ndarray | None = None
+    wrap: WrapOperators | None = None
+
+    def solve_interface(self, rhs):
+        from scipy.linalg import lu_solve
+        return lu_solve(self.lu_piv, rhs)
+
+    def retained_floats(self) -> int:
+        total = self.lu_piv[0].size + self.s_gi_ge.size + self.t_ei.size
+        if self.wrap is not None:
+            total += self.wrap.p_up.size + self.wrap.p_down.size
+        return total
+
+
+def _leaf_host_ops(solver, grp, slot) -> LeafOperators:
+    """Reference-layout operators of one leaf from its group's device tensors."""
+    sc, m, b, P = grp.sc, (solver.p - 2) ** 2, 4 * solver.q, solver.p ** 2
+    fs = grp.fs[slot].cpu().numpy()
+    h = grp.h[slot].cpu().numpy()
+    perm = grp.perm[slot].cpu().numpy().astype(np.int64)
+    S = np.empty((P, b))
+    S[sc.i_ce] = sc.lift
+    S[sc.i_ci] = fs[:, m:]
+    F = np.zeros((P, m))
+    F[np.ix_(sc.i_ci, perm)] = fs[:, :m]       # inv[:, perm[j]] = M[:, j]
+    H = np.empty((b, m))
+    H[:, perm] = h
+    return LeafOperators(S=S, T=None, F=F, H=H)
+
+
+class _LeafOpsView(Mapping):
+    def __init__(self, solver):
+        self._s = solver
+
+    def __getitem__(self, nid):
+        s = self._s
+        if s.mode == "econ" or int(nid) not in s.leaf_loc:
+            raise KeyError(nid)
+        gi, slot = s.leaf_loc[int(nid)]
+        return _leaf_host_ops(s, s.leaf_groups[gi], slot)
+
+    def __iter__(self):
+        return iter(() if self._s.mode == "econ" else sorted(self._s.leaf_loc))
+
+    def __len__(self):
+        return 0 if self._s.mode == "econ" else len(self._s.leaf_loc)
+
+
+class _ParentOpsView(Mapping):
+    def __init__(self, solver):
+        self._s = solver
+        self._loc = {int(n): (g, i) for g in solver.parent_groups for i, n in enumerate(g.ids)}
+
+    def __getitem__(self, nid):
+        grp, slot = self._loc[int(nid)]
+        s = self._s
+        lu_piv = s._interface_factors()[int(nid)]
+        m3 = grp.m3
+        tei = grp.tei[slot].cpu().numpy()
+        if grp.wrap is not None:
+            en = s.plan.node[int(nid)]
+            S = grp.wrap["xsw"][:, m3:].cpu().numpy()
+            wrap = WrapOperators(p_up=grp.wrap["pu"], p_down=grp.wrap["pd"], perm=en.wrap.perm, fine=en.wrap.fine)
+            return ParentOperators(lu_piv=lu_piv, s_gi_ge=S, t_ei=tei, wrap=wrap)
+        return ParentOperators(lu_piv=lu_piv, s_gi_ge=grp.xs[slot, :, m3:].cpu().numpy(), t_ei=tei)
+
+    def __iter__(self):
+        return iter(sorted(self._loc))
+
+    def __len__(self):
+        return len(self._loc)
+
+
 class _HostLease:
     """numpy base object for a lent page-locked result buffer (FactorizedSolver._out_buffers):
     arrays built from it keep it alive, and its death returns the buffer to the ring."""
@@ -176,6 +280,7 @@ class _ParentGroup:
     perm: torch.Tensor = None  # [npar, m3] column order of X (pivot order)
     y: torch.Tensor = None     # [npar, e, m3] T_ei X, solve-time operator (FactorizedSolver._prepare)
     wrap: dict = None      # singleton wrapped parent: qd, qu, pu, pd, ec, xsw, tw
+    delta: torch.Tensor = None  # [npar, m3, m3] interface block (only when built for the archive view)
 
     @property
     def e(self):
@@ -200,6 +305,39 @@ class FactorizedSolver:
         # the device vector pool and captured graphs are per solver, so host-API solves from
         # several threads are serialised here and each one returns its own host arrays
         self._lock = threading.RLock()
+
+    # -- per-node operator views (reference solver.py:224-225, archive.py:47-62) ---------------
+    @property
+    def leaf_ops(self):
+        """leaf id -> LeafOperators(S (P x 4q), T=None, F (P x m), H (4q x m)) in the reference's
+        layout (leaf.py:124-163), materialised on the host on access. Empty in economy mode, as
+        in the reference (only stored mode retains leaf operators)."""
+        return _LeafOpsView(self)
+
+    @property
+    def parent_ops(self):
+        """box id -> ParentOperators(lu_piv, s_gi_ge, t_ei, wrap) in the reference's layout
+        (solver.py:77-105). The device keeps X = Delta^-1 explicitly; the reference's LAPACK
+        (lu, piv) of Delta is produced on first access (one device rebuild that keeps the
+        interface blocks, then scipy lu_factor per box) and cached."""
+        return _ParentOpsView(self)
+
+    def _interface_factors(self) -> dict:
+        cached = getattr(self, "_lu_cache", None)
+        if cached is not None:
+            return cached
+        from scipy.linalg import lu_factor
+        tmp = FactorizedSolver(self.tree, self.plan, self.spec, self.p, self.q, self.mode)
+        _build_device(tmp, list(range(len(self.tree.nodes) - 1, -1, -1)), keep_delta=True)
+        out = {}
+        for grp in tmp.parent_groups:
+            d = grp.delta.cpu().numpy()
+            for slot, nid in enumerate(grp.ids):
+                lu, piv = lu_factor(d[slot])
+                out[int(nid)] = (lu, piv.astype(np.int32))
+        del tmp
+        self._lu_cache = out
+        return out
 
     # -- accounting -------------------------------------------------------------------------
     def leaf_memory_floats(self) -> int:
@@ -1005,7 +1143,7 @@ class _Phases:
                 for i in range(len(self.marks) - 1)]
 
 
-def _build_device(solver: FactorizedSolver, order, profile=False):
+def _build_device(solver: FactorizedSolver, order, profile=False, keep_delta=False):
     lib = _ext.load()
     ph = _Phases(profile)
     ph.mark("start")
@@ -1077,10 +1215,13 @@ def _build_device(solver: FactorizedSolver, order, profile=False):
             grp.status = torch.zeros(npar, dtype=torch.int32, device=dev)
             grp.perm = torch.empty((npar, m3), dtype=torch.int32, device=dev)
             ws = torch.empty(int(lib.hps_merge_workspace_bytes(npar, m3, e)), dtype=torch.uint8, device=dev)
+            if keep_delta:
+                grp.delta = torch.empty((npar, m3, m3), dtype=torch.float64, device=dev)
             mb = _ext.MergeBatch(npar, m3, grp.n1, grp.n2, ta_ptr.data_ptr(), tb_ptr.data_ptr(), grp.lda, grp.ldb,
                                  idx.data_ptr(), 0 if same else idx.shape[1], grp.xs.data_ptr(),
                                  grp.tei.data_ptr(), grp.tnew.data_ptr(), grp.dnorm.data_ptr(),
-                                 grp.xnorm.data_ptr(), grp.status.data_ptr(), grp.perm.data_ptr(), ws.data_ptr())
+                                 grp.xnorm.data_ptr(), grp.status.data_ptr(), grp.perm.data_ptr(), ws.data_ptr(),
+                                 grp.delta.data_ptr() if keep_delta else 0)
             ph.mark(f"merge-prep d{d}")
             _ext.check(lib.hps_merge_build(mb, s), "merge build")
             ph.mark(f"merge d{d} x{npar} m3={m3} e={e}")
@@ -1108,6 +1249,47 @@ def _build_device(solver: FactorizedSolver, order, profile=False):
         else:
             grp.coef = None
     solver._layout = _layout(solver)
+
+
+def _skeleton(solver: FactorizedSolver):
+    """Leaf and parent groups of `solver` with the same grouping, order and leaf rows as
+    _build_device, but no operators: the archive loader fills them from per-node sections."""
+    tree, plan, p, q = solver.tree, solver.plan, solver.p, solver.q
+    dev = solver.device
+    tables = _plan_tables(tree, plan)
+    row, leaf_ids = 0, []
+    for key, ids in tables["leaf_groups"].items():
+        sc = shape_constants(p, q, float(key[0]), float(key[1]))
+        grp = _LeafGroup(key, ids, sc, first_row=row)
+        L = len(ids)
+        row += L
+        leaf_ids.extend(ids)
+        grp.consts = _leaf_consts(sc, dev)
+        grp.anorm = torch.empty(L, dtype=torch.float64, device=dev)
+        grp.ainvnorm = torch.empty(L, dtype=torch.float64, device=dev)
+        grp.status = torch.zeros(L, dtype=torch.int32, device=dev)
+        for slot, nid in enumerate(ids):
+            solver.leaf_loc[nid] = (len(solver.leaf_groups), slot)
+        solver.leaf_groups.append(grp)
+    solver._leaf_ids = leaf_ids
+    solver._n_leaves = len(leaf_ids)
+    solver.depth = tables["depth"]
+    for d, _level_ids, level_groups in tables["levels"]:
+        for ids, _rows_idx, _same in level_groups:
+            en0 = plan.node[ids[0]]
+            ca0, cb0 = tree.nodes[ids[0]].children
+            solver.parent_groups.append(_ParentGroup(d, ids, en0.j3.size, en0.pos1_a.size, en0.pos2_b.size,
+                                                     plan.node[ca0].ext.size, plan.node[cb0].ext.size))
+    return tables
+
+
+def _leaf_coefficients(solver, grp):
+    """[6, L, P] coefficient samples of a leaf group, evaluated on the device (economy mode)."""
+    dev = solver.device
+    org = _f64(np.array([[solver.tree.nodes[n].bounds.x1lo, solver.tree.nodes[n].bounds.x2lo] for n in grp.ids]),
+               dev)
+    pts = _f64(grp.sc.cheb2d(), dev)[None, :, :] + org[:, None, :]
+    return coeff_mod.evaluate(solver.spec.coefficients, pts).contiguous()
 
 
 def _leaf_consts(sc, dev):

@@ -361,6 +361,28 @@ def resonance_fixture():
          box=np.array([box]), lam=np.array([fb]))
 
 
+def archive_fixture():
+    """Archives written by the reference's own persist_operators (archive.py:65-101), stored and
+    economy mode on a refined mesh (wrapped parents), plus the reference's solves from the
+    reloaded solvers, for the GPU loader's interop test."""
+    from specdtn.archive import load_operators, persist_operators
+    for mode in ("stored", "econ"):
+        tree = build_uniform_tree(UNIT, 2)
+        refine_near_point(tree, RefinementSpec((0.1, 0.1), 1))
+        solver = build_stage(tree, catalog("manufactured", u="sin(pi*x1)*sin(pi*x2)"), 9, 8, mode)
+        path = os.path.join(HERE, f"ref_archive_{mode}.sdtn")
+        persist_operators(solver, path)
+        loaded = load_operators(path)
+        st = loaded.solve()
+        g = {lf.id: np.cos(np.arange((9 - 2) ** 2) * 0.1 + lf.id) for lf in tree.leaves()}
+        st2 = loaded.solve(f=lambda pts: pts[:, 0] * pts[:, 1], g=g)
+        a = state_arrays(st, loaded)
+        for k, v in state_arrays(st2, loaded).items():
+            a["fg_" + k] = v
+        save(f"ref_archive_{mode}_solution.npz", **a)
+        print(f"ref_archive_{mode}.sdtn: {os.path.getsize(path) / 1024:.1f} KiB")
+
+
 def fullsize_fixture():
     """BASELINE configs 2-5 at their full sizes, run by the reference itself. The full solutions
     are too large to commit, so the fixture keeps a fingerprint: norms of u, u on 2000 seeded
@@ -420,6 +442,9 @@ if __name__ == "__main__":
         raise SystemExit
     if "--only-plans" in _sys.argv:
         plan_fixture()
+        raise SystemExit
+    if "--only-archive" in _sys.argv:
+        archive_fixture()
         raise SystemExit
     if "--only-resonance" in _sys.argv:
         resonance_fixture()

@@ -33,7 +33,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned ph) {
 
 // per item: nbox boxes; box b of item i at coords given by the layout
 __global__ void __launch_bounds__(288, 1) stream_kernel(const __grid_constant__ CUtensorMap tm, int layout, int nitems,
-                                                         int R, int nbox, int box_bytes, int ns, double* sink) {
+                                                         int R, int nbox, int box_bytes, int tx_bytes, int ns,
+                                                         double* sink) {
   extern __shared__ unsigned char raw[];
   unsigned char* base = (unsigned char*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(base + (size_t)ns * box_bytes);
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(288, 1) stream_kernel(const __grid_constant__ 
       for (int item = blockIdx.x; item < nitems; item += gridDim.x)
         for (int b = 0; b < nbox; ++b) {
           if (!first) mbar_wait(empty + slot, ph ^ 1u);
-          mbar_expect_tx(full + slot, box_bytes);
+          mbar_expect_tx(full + slot, tx_bytes);
           void* dst = base + (size_t)slot * box_bytes;
           if (layout == 0) {
             asm volatile(
@@ -158,7 +159,8 @@ int main(int argc, char** argv) {
       cudaEventCreate(&e1);
       for (int rep = 0; rep < 2; ++rep) {
         cudaEventRecord(e0);
-        stream_kernel<<<sms, 288, smem>>>(tm, layout, nitems, R, nbox, box_bytes, ns, sink);
+        const int tx = layout == 2 ? (R / 4) * 4 * 128 : R * 128;  // bytes one box delivers
+        stream_kernel<<<sms, 288, smem>>>(tm, layout, nitems, R, nbox, box_bytes, tx, ns, sink);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
       }
