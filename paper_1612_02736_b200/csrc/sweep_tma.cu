@@ -29,9 +29,8 @@ namespace hps {
 
 namespace {
 
-constexpr int TM_CONSUMERS = 8;
-constexpr int TM_THREADS = 32 * (TM_CONSUMERS + 1);
-constexpr int TM_MAXT = 4;  // m-tiles per consumer warp (R <= 256)
+// NC consumer warps (template parameter, 8 or 16) + 1 producer warp; a consumer warp owns up to
+// 32 / NC m-tiles of 8 rows (R <= 256)
 
 __device__ __forceinline__ uint32_t tma_smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -74,15 +73,16 @@ __device__ __forceinline__ void dmma_nv(double& d0, double& d1, double a, double
       : "+d"(d0), "+d"(d1)
       : "d"(a), "d"(b));
 }
-__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(TM_CONSUMERS * 32) : "memory"); }
+template <int NC>
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(NC * 32) : "memory"); }
 
 
 }  // namespace
 
 // One pipeline stage of MMAs for a warp owning T m-tiles (tile = warp + 8 i): SPS slabs of 16
 // columns, 4 k4-steps each; even / odd k4 steps accumulate into separate sets.
-template <int T, int NT, int XLD, int SPS>
-__device__ __forceinline__ void stage_mma(double (&acc)[2][TM_MAXT][NT][2], const unsigned char* base, int slot,
+template <int T, int NT, int XLD, int SPS, int NC, int MT>
+__device__ __forceinline__ void stage_mma(double (&acc)[2][MT][NT][2], const unsigned char* base, int slot,
                                           int sb_bytes, int nq, const double* xc, int k0, const int (&aoff)[4],
                                           int warp, int g, int t) {
 #pragma unroll
@@ -97,7 +97,7 @@ __device__ __forceinline__ void stage_mma(double (&acc)[2][TM_MAXT][NT][2], cons
       for (int n = 0; n < NT; ++n) bv[n] = xc[kk * XLD + n * 8 + g];
       double av[T];
 #pragma unroll
-      for (int i = 0; i < T; ++i) av[i] = slab[(warp + i * TM_CONSUMERS) * 128 + aoff[k4]];
+      for (int i = 0; i < T; ++i) av[i] = slab[(warp + i * NC) * 128 + aoff[k4]];
 #pragma unroll
       for (int i = 0; i < T; ++i)
 #pragma unroll
@@ -106,12 +106,14 @@ __device__ __forceinline__ void stage_mma(double (&acc)[2][TM_MAXT][NT][2], cons
   }
 }
 
-constexpr int TM_GMAX = 12;  // x-gather copy units per consumer thread
+constexpr int TM_GUNITS = 12 * 256;  // x-gather copy units per CTA (K * units per row)
 
-template <int NRP, int SPS>
-__global__ void __launch_bounds__(TM_THREADS, 1)
+template <int NRP, int SPS, int NC>
+__global__ void __launch_bounds__(32 * (NC + 1), 1)
     gemv_tma_kernel(const __grid_constant__ CUtensorMap tm, GemvArgs a, int ns, int kst, int sb_bytes) {
   constexpr int sps = SPS;
+  constexpr int MT = 32 / NC;                // m-tiles per consumer warp
+  constexpr int TM_GMAX = TM_GUNITS / (NC * 32);  // x-gather copy units per consumer thread
   extern __shared__ unsigned char smraw[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   constexpr int XLD = NRP + 4;
@@ -130,14 +132,14 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, TM_CONSUMERS);
+      mbar_init(empty + s, NC);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   pdl_trigger();
 
-  if (warp == TM_CONSUMERS) {
+  if (warp == NC) {
     // ---- producer: operator slabs never depend on the previous kernel, start right away
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm) : "memory");
@@ -170,7 +172,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   int urow[TM_GMAX], ucol[TM_GMAX];
 #pragma unroll
   for (int u = 0; u < TM_GMAX; ++u) {
-    const int e = tid + u * TM_CONSUMERS * 32;
+    const int e = tid + u * NC * 32;
     urow[u] = e < nunits ? e / upr : -1;
     ucol[u] = e < nunits ? (e - (e / upr) * upr) * (wide ? 2 : 1) : 0;
   }
@@ -194,8 +196,8 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
 
-  for (int e = tid; e < 2 * kp * XLD; e += TM_CONSUMERS * 32) xbuf[e] = 0.0;
-  consumers_sync();
+  for (int e = tid; e < 2 * kp * XLD; e += NC * 32) xbuf[e] = 0.0;
+  consumers_sync<NC>();
   pdl_wait();  // the pool (x) is produced by the previous step
   if (blockIdx.x < a.nitems) {
     load_idx(blockIdx.x);
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   // index loads nor the copies sit on the consumers' critical path
   if (blockIdx.x + gridDim.x < a.nitems) load_idx(blockIdx.x + gridDim.x);
   asm volatile("cp.async.wait_all;\n" ::: "memory");
-  consumers_sync();
+  consumers_sync<NC>();
 
   // A fragment rows: lanes g = 0..3 take even rows, 4..7 odd rows of an 8-row tile, so both
   // half-warps read 8 distinct 16-byte chunks of the 128B-swizzled slab (no bank conflicts)
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     aoff[k4] = rg * 16 + ((((c >> 1) ^ rg) << 1) | (c & 1));
   }
   const int mt = (R + 7) >> 3;
-  const int ntw = warp < mt ? (mt - warp + TM_CONSUMERS - 1) / TM_CONSUMERS : 0;  // m-tiles of this warp
+  const int ntw = warp < mt ? (mt - warp + NC - 1) / NC : 0;  // m-tiles of this warp
   int slot = 0;
   unsigned ph = 0;
   int it = 0;
@@ -225,11 +227,11 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     const double* xc = xbuf + (size_t)(it & 1) * kp * XLD;
     double* xn = xbuf + (size_t)((it + 1) & 1) * kp * XLD;
     // two accumulator sets (even / odd k4 steps): twice the independent DMMA chains per warp
-    double acc[2][TM_MAXT][NT][2];
+    double acc[2][MT][NT][2];
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int i = 0; i < TM_MAXT; ++i)
+      for (int i = 0; i < MT; ++i)
 #pragma unroll
         for (int n = 0; n < NT; ++n) acc[h][i][n][0] = acc[h][i][n][1] = 0.0;
     const int nxt = item + gridDim.x;
@@ -238,10 +240,10 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     // output rows of this item, loaded ahead of the epilogue
     const int* oi = a.oidx + (long long)item * a.ostride;
     const int* ai = a.aidx ? a.aidx + (long long)item * a.ostride : nullptr;
-    int orows[TM_MAXT], arows[TM_MAXT];
+    int orows[MT], arows[MT];
 #pragma unroll
-    for (int i = 0; i < TM_MAXT; ++i) {
-      const int r = (warp + i * TM_CONSUMERS) * 8 + rg;
+    for (int i = 0; i < MT; ++i) {
+      const int r = (warp + i * NC) * 8 + rg;
       orows[i] = r < R ? __ldg(oi + r) : 0;
       arows[i] = (ai && r < R) ? __ldg(ai + r) : -1;
     }
@@ -251,10 +253,10 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
       // the tile count is warp-uniform: dispatch to a branch-free body per count (a guarded
       // DMMA compiles to a predicated one, which still occupies the tensor pipe)
       switch (ntw) {
-        case 1: stage_mma<1, NT, XLD, SPS>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
-        case 2: stage_mma<2, NT, XLD, SPS>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
-        case 3: stage_mma<3, NT, XLD, SPS>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
-        case 4: stage_mma<4, NT, XLD, SPS>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
+        case 1: stage_mma<1, NT, XLD, SPS, NC, MT>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
+        case 2: stage_mma<(MT >= 2 ? 2 : 1), NT, XLD, SPS, NC, MT>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
+        case 3: stage_mma<(MT >= 3 ? 3 : 1), NT, XLD, SPS, NC, MT>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
+        case 4: stage_mma<(MT >= 4 ? 4 : 1), NT, XLD, SPS, NC, MT>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
         default: break;
       }
       __syncwarp();
@@ -266,8 +268,8 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     }
     // epilogue: y rows -> pool (+ add rows)
 #pragma unroll
-    for (int i = 0; i < TM_MAXT; ++i) {
-      const int r = (warp + i * TM_CONSUMERS) * 8 + rg;
+    for (int i = 0; i < MT; ++i) {
+      const int r = (warp + i * NC) * 8 + rg;
       if (r >= R) continue;
       const long long orow = (long long)orows[i] * nrhs;
       const long long arow = arows[i] >= 0 ? (long long)arows[i] * nrhs : -1;
@@ -289,7 +291,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
       const int ld2 = a.A2.ld, K2 = a.K2, R2 = a.R2, x0 = K - K2;
       const int* o2 = a.o2idx + (long long)item * R2;
       const int* a2 = a.a2idx ? a.a2idx + (long long)item * R2 : nullptr;
-      for (int tile = warp; tile * 8 < R2; tile += TM_CONSUMERS) {
+      for (int tile = warp; tile * 8 < R2; tile += NC) {
         const int ra = tile * 8 + g;
         const double* arow2 = A2 + (long long)(ra < R2 ? ra : 0) * ld2;
         double c2[NT][2];
@@ -333,7 +335,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
       }
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
-    consumers_sync();  // next X landed for everyone; this X no longer read
+    consumers_sync<NC>();  // next X landed for everyone; this X no longer read
   }
 }
 
@@ -370,13 +372,17 @@ bool launch_gemv_tma(const GemvArgs& a, cudaStream_t s) {
   if (a.nrhs <= 2 || a.nrhs > 16 || a.x2idx || a.A.ptrs || a.mode2 == 2) return false;
   // the leaf downward step (R = (p-2)^2 >= 128 rows); shorter operators (leaf upward, R = 4q)
   // measured faster on the register-streaming kernel, whose 32 warps/SM hide more latency
-  if (a.R < 128 || a.R > 256 || a.K < 16 || a.nitems < 148) return false;
+  static const int min_r = [] {  // HPS_TMA_MINR: shortest operator routed here
+    const char* e = getenv("HPS_TMA_MINR");
+    return e ? atoi(e) : 128;
+  }();
+  if (a.R < min_r || a.R > 256 || a.K < 16 || a.nitems < 148) return false;
   if (a.A.stride != (long long)a.R * a.A.ld || (a.A.ld * 8) % 16 != 0) return false;
   const double* gbase = a.A.base + a.A.off;
   if (reinterpret_cast<uintptr_t>(gbase) % 16 != 0) return false;
   if (a.mode2 == 1 && (a.K2 > a.K || a.R2 <= 0)) return false;
   const int upr = a.nrhs % 2 == 0 ? a.nrhs / 2 : a.nrhs;
-  if ((long long)a.K * upr > 12LL * 256) return false;  // TM_GMAX units per consumer thread
+  if ((long long)a.K * upr > TM_GUNITS) return false;  // x-gather copy units per CTA
   if (a.nrhs % 2 == 0 && reinterpret_cast<uintptr_t>(a.pool) % 16 != 0) return false;
   auto enc = encode_fn();
   if (!enc) return false;
@@ -414,8 +420,14 @@ bool launch_gemv_tma(const GemvArgs& a, cudaStream_t s) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = a.nitems < sms ? a.nitems : sms;
+  // consumer warps per CTA (HPS_TMA_NC = 8 or 16): 16 puts 4 DMMA warps on each SM sub-partition
+  static const int nc = [] {
+    const char* e = getenv("HPS_TMA_NC");
+    return (e && atoi(e) == 8) ? 8 : 16;
+  }();
   using KFn = void (*)(const CUtensorMap, GemvArgs, int, int, int);
-  const KFn k = nrp == 16 ? gemv_tma_kernel<16, 1> : gemv_tma_kernel<8, 1>;
+  const KFn k = nc == 16 ? (nrp == 16 ? gemv_tma_kernel<16, 1, 16> : gemv_tma_kernel<8, 1, 16>)
+                         : (nrp == 16 ? gemv_tma_kernel<16, 1, 8> : gemv_tma_kernel<8, 1, 8>);
   static bool configured[2] = {};
   if (!configured[nrp == 16]) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
@@ -423,7 +435,7 @@ bool launch_gemv_tma(const GemvArgs& a, cudaStream_t s) {
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(TM_THREADS);
+  cfg.blockDim = dim3(32 * (nc + 1));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
