@@ -152,6 +152,9 @@ typedef struct {
   hps_mat_batch A2;
   const int* a2idx;
   const int* o2idx;
+  int kparts;           /* 0/1: item i is A_i (R x K). kparts > 1 (split-K): item i is the column
+                           block [(i % kparts) K, (i % kparts + 1) K) of operator A_{i / kparts},
+                           which A describes unsplit (base/stride/ld/off, no ptrs) */
 } hps_gemv_batch;
 int hps_sweep_gemv(const hps_gemv_batch* g, void* stream);
 

@@ -44,7 +44,7 @@ class GemvBatch(C.Structure):
                 ("A", MatBatch), ("pool", C.c_void_p), ("xidx", C.c_void_p),
                 ("x2idx", C.c_void_p), ("aidx", C.c_void_p), ("oidx", C.c_void_p),
                 ("mode2", C.c_int), ("R2", C.c_int), ("K2", C.c_int), ("A2", MatBatch),
-                ("a2idx", C.c_void_p), ("o2idx", C.c_void_p)]
+                ("a2idx", C.c_void_p), ("o2idx", C.c_void_p), ("kparts", C.c_int)]
 
 
 class LeafApplyArgs(C.Structure):

@@ -218,6 +218,8 @@ static int to_gemv_args(const hps_gemv_batch* gb, GemvArgs* out) {
   a.o2idx = gb->o2idx;
   a.xstride = a.K;
   a.ostride = a.R;
+  a.kparts = gb->kparts > 1 ? gb->kparts : 1;
+  if (a.kparts > 1 && (gb->A.ptrs || a.nitems % a.kparts)) return HPS_EINVAL;
   // HPS_PRE_INDEX (read once per process, host side only): bit mask of the kernels that load
   // their static gather indices before the programmatic-launch wait; a kernel argument, so no
   // device-symbol copy (and no legacy-stream work) ever happens inside a launch path

@@ -102,10 +102,17 @@ struct GemvArgs {
   long long ostride;
   int pre_mask;      // which kernels load static gather indices before the launch wait
                      // (bit mask, HPS_PRE_INDEX, set per launch by launch_gemv_gather)
+  int kparts;        // split-K: item i = column block i % kparts of operator i / kparts (ABI)
 };
+// Operator rows of item i (split-K aware)
+__device__ __forceinline__ const double* gemv_a(const GemvArgs& a, int i) {
+  return a.kparts > 1 ? a.A.get(i / a.kparts) + (long long)(i % a.kparts) * a.K : a.A.get(i);
+}
 int launch_gemv_gather(const GemvArgs& a, cudaStream_t s);
 // TMA-fed multi-RHS path for large leaf levels (sweep_tma.cu); false = not applicable
 bool launch_gemv_tma(const GemvArgs& a, cudaStream_t s);
+// TMA-streamed multi-RHS path for large operator items (top levels, split-K parts; sweep_tma.cu)
+bool launch_gemv_stream(const GemvArgs& a, cudaStream_t s);
 
 // Leaf operator application for time stepping (leaf_apply.cu)
 struct LeafApplyArgs {

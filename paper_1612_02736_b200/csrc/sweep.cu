@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(SW_THREADS) gemv_gather_kernel(GemvArgs a, int
   const int R = a.R, K = a.K, nrhs = a.nrhs;
   const int r0 = blockIdx.x * rows_per_cta;
   const int r1 = min(R, r0 + rows_per_cta);
-  const double* Ai = a.A.get(item);
+  const double* Ai = gemv_a(a, item);
   const long long lda = a.A.ld;
   const int* xi = a.xidx + (long long)item * a.xstride;
   const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(256, 4) gemv_dmma_kernel(GemvArgs a, int rpc, 
   double* red = xs + (size_t)kchunk * XLD;
   const int R = a.R, K = a.K, nrhs = a.nrhs;
   const int rbase = blockIdx.x * rpc + wr * 16;
-  const double* Ai = a.A.get(item);
+  const double* Ai = gemv_a(a, item);
   const long long lda = a.A.ld;
   const int* xi = a.xidx + (long long)item * a.xstride;
   const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(256) gemv_dmma_multi_kernel(GemvArgs a) {
     __syncwarp();
   else
     asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(GW * 32) : "memory");
-  const double* Ai = a.A.get(item);
+  const double* Ai = gemv_a(a, item);
   const long long lda = a.A.ld;
   const int* ai = a.aidx ? a.aidx + (long long)item * a.ostride : nullptr;
   const int* oi = a.oidx + (long long)item * a.ostride;
@@ -662,7 +662,7 @@ __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chun
   const int* xi = a.xidx + (long long)item * a.xstride;
   const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
   const double* pool = a.pool;
-  const double* Ai = a.A.get(item);
+  const double* Ai = gemv_a(a, item);
   const int r0 = chunk * rows_per_cta;
   const int r1 = min(a.R, r0 + rows_per_cta);
   __shared__ __align__(8) uint64_t sa_bar;
@@ -775,7 +775,7 @@ __global__ void __launch_bounds__(256) sweep_multi_kernel(GemvArgs a, int batch_
   __shared__ __align__(8) uint64_t sa_bars[IPC];
   pdl_trigger();
   const bool live = item < a.nitems;
-  const double* Ai = live ? a.A.get(item) : nullptr;
+  const double* Ai = live ? gemv_a(a, item) : nullptr;
   int shift = 0;
   if (SA && live) {
     const uintptr_t src = reinterpret_cast<uintptr_t>(Ai);
@@ -973,7 +973,7 @@ static bool launch_sweep(const GemvArgs& a, cudaStream_t s) {
       msa = e ? atoi(e) : 1;
     }
     const size_t tile = sizeof(double) * (size_t)sa_tile_doubles(a.R, a.A.ld);
-    const bool sa = msa && a.A.ptrs == nullptr && tile <= 40 * 1024;  // larger items fall back to ipc = 1
+    const bool sa = msa && a.A.ptrs == nullptr && a.kparts <= 1 && tile <= 40 * 1024;  // larger: ipc = 1
     const size_t per_item = smem + (sa ? tile : 0);
     if (multi && gx == 1 && (a.mode2 == 0 || a.mode2 == 3)) {
       // next ipc: the level still gives min_ctas CTAs, x (and the tiles) fit, and the group's
@@ -1070,7 +1070,7 @@ __global__ void __launch_bounds__(256) gemv_row1_kernel(GemvArgs a) {
     }
   }
   if (!live) return;
-  const double* A = a.A.get(item);
+  const double* A = gemv_a(a, item);
   double acc = 0.0;
 #pragma unroll
   for (int k = 0; k < KP; ++k) {
@@ -1101,6 +1101,7 @@ int launch_gemv_gather(const GemvArgs& a, cudaStream_t s) {
     if (ok) return cudaGetLastError() == cudaSuccess ? 0 : 2;
   }
   if (a.nrhs > 2 && launch_gemv_tma(a, s)) return cudaGetLastError() == cudaSuccess ? 0 : 2;
+  if (a.nrhs > 2 && launch_gemv_stream(a, s)) return cudaGetLastError() == cudaSuccess ? 0 : 2;
   if (a.nrhs > 2 && a.nrhs <= 16 && a.R > 1 && !a.A.ptrs) {
     const bool ok = a.nrhs <= 8 ? launch_dmma_multi<8>(a, s) : launch_dmma_multi<16>(a, s);
     if (ok) return cudaGetLastError() == cudaSuccess ? 0 : 2;

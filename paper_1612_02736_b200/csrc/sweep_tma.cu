@@ -115,7 +115,10 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1)
   constexpr int MT = 32 / NC;                // m-tiles per consumer warp
   constexpr int TM_GMAX = TM_GUNITS / (NC * 32);  // x-gather copy units per consumer thread
   extern __shared__ unsigned char smraw[];
-  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned (128B swizzle) by pointer arithmetic on the shared array itself: a round
+  // trip through an integer would lose the address space and turn every fragment load into a
+  // generic LD instead of LDS
+  unsigned char* base = smraw + ((1024u - (tma_smem_addr(smraw) & 1023u)) & 1023u);
   constexpr int XLD = NRP + 4;
   constexpr int NT = NRP / 8;
   const int R = a.R, K = a.K, nrhs = a.nrhs;
@@ -369,7 +372,7 @@ bool tma_enabled() {
 // Returns true when the step was launched here; false leaves it to the generic kernels.
 bool launch_gemv_tma(const GemvArgs& a, cudaStream_t s) {
   if (!tma_enabled()) return false;
-  if (a.nrhs <= 2 || a.nrhs > 16 || a.x2idx || a.A.ptrs || a.mode2 == 2) return false;
+  if (a.nrhs <= 2 || a.nrhs > 16 || a.x2idx || a.A.ptrs || a.kparts > 1 || a.mode2 == 2) return false;
   // the leaf downward step (R = (p-2)^2 >= 128 rows); shorter operators (leaf upward, R = 4q)
   // measured faster on the register-streaming kernel, whose 32 warps/SM hide more latency
   static const int min_r = [] {  // HPS_TMA_MINR: shortest operator routed here
@@ -444,6 +447,348 @@ bool launch_gemv_tma(const GemvArgs& a, cudaStream_t s) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k, tm, a, ns, kst, sb) == cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Multi-RHS (3..16) steps with LARGE operator items (top tree levels, split-K parts): the
+// operator is streamed by TMA in row blocks of RB <= 256 rows, so every item size maps onto
+// one persistent CTA per SM with ~150 KB of operator in flight.
+//
+// Units = (item, row block); item i may be a split-K part (kparts > 1: column block i % kparts
+// of operator i / kparts), described to TMA as (row, column) coordinates in one 2D view of the
+// whole operator array. Warp roles per CTA:
+//   warp 8       producer: 16-column slabs of the unit's RB rows -> smem ring (128B swizzle)
+//   warps 9..10  gather:   x chunks of KX columns (x = pool[xidx] - pool[x2idx], zero padded)
+//                          -> a double-buffered smem ring, with the x2 difference applied
+//   warps 0..7   DMMA consumers, 4 m-tiles of 8 rows each (tile w, w+8, w+16, w+24)
+// mode2 = 3 (parent downward [X | S][d; u_ext]): columns < K2 accumulate into one accumulator
+// set, the rest into the other; w3 = the first, u3 = their sum. Otherwise the two sets take
+// alternating k4 steps (two independent DMMA chains per tile).
+// Why: the register-streaming gemv_dmma_kernel kept ~16 KB per SM in flight and ran the config-5
+// top levels at 0.2-2.5 TB/s (root downward partials: 147 MB in 123 us).
+constexpr int ST_NC = 8, ST_GW = 4, ST_THREADS = 32 * (ST_NC + 1 + ST_GW);
+
+struct StreamCfg {
+  int RB, nrb, KX, ns, sb_bytes;
+};
+
+// one k4 step of T m-tiles into accumulator set h
+template <int T, int NT>
+__device__ __forceinline__ void stream_k4(double (&acc)[2][4][NT][2], int h, const double* slab, int warp, int aoff,
+                                          const double (&bv)[NT]) {
+  double av[T];
+#pragma unroll
+  for (int i = 0; i < T; ++i) av[i] = slab[(warp + i * ST_NC) * 128 + aoff];
+  if (h == 0) {
+#pragma unroll
+    for (int i = 0; i < T; ++i)
+#pragma unroll
+      for (int n = 0; n < NT; ++n) dmma_nv(acc[0][i][n][0], acc[0][i][n][1], av[i], bv[n]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < T; ++i)
+#pragma unroll
+      for (int n = 0; n < NT; ++n) dmma_nv(acc[1][i][n][0], acc[1][i][n][1], av[i], bv[n]);
+  }
+}
+
+template <int NRP>
+__global__ void __launch_bounds__(ST_THREADS, 1)
+    gemv_stream_kernel(const __grid_constant__ CUtensorMap tm, GemvArgs a, StreamCfg c) {
+  extern __shared__ unsigned char smraw[];
+  unsigned char* base = smraw + ((1024u - (tma_smem_addr(smraw) & 1023u)) & 1023u);
+  constexpr int XLD = NRP + 4;
+  constexpr int NT = NRP / 8;
+  const int R = a.R, K = a.K, nrhs = a.nrhs, RB = c.RB, KX = c.KX, ns = c.ns;
+  const int kp = a.kparts > 1 ? a.kparts : 1;
+  const int nslab = (K + 15) >> 4, nchunk = (K + KX - 1) / KX, spc = KX >> 4;
+  const long long units = (long long)a.nitems * c.nrb;
+  double* xbuf = reinterpret_cast<double*>(base + (size_t)ns * c.sb_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + 2 * (size_t)KX * XLD);
+  uint64_t* empty = full + ns;
+  uint64_t* xfull = empty + ns;
+  uint64_t* xempty = xfull + 2;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < ns; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, ST_NC);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(xfull + i, ST_GW * 32);
+      mbar_init(xempty + i, ST_NC);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  pdl_trigger();
+
+  if (warp == ST_NC) {
+    // ---- producer: static operator, streams before the launch wait
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm) : "memory");
+      int slot = 0;
+      unsigned ph = 0;
+      bool first = true;
+      const unsigned tx = (unsigned)RB * 128u;
+      for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+        const int item = (int)(u / c.nrb), rb = (int)(u - (long long)item * c.nrb);
+        const int row0 = (item / kp) * R + rb * RB, col0 = (item % kp) * K;
+        for (int j = 0; j < nslab; ++j) {
+          if (!first) mbar_wait(empty + slot, ph ^ 1u);
+          mbar_expect_tx(full + slot, tx);
+          tma_load_2d(base + (size_t)slot * c.sb_bytes, &tm, col0 + j * 16, row0, full + slot);
+          if (++slot == ns) {
+            slot = 0;
+            ph ^= 1u;
+            first = false;
+          }
+        }
+      }
+    }
+    return;
+  }
+  if (warp > ST_NC) {
+    // ---- gather: x chunks (pool rows written by the previous step: after the launch wait)
+    pdl_wait();
+    const int gt = tid - (ST_NC + 1) * 32;
+    const int upr = nrhs / 2 + (nrhs & 1);  // two RHS per copy unit
+    int xs = 0;
+    unsigned xph = 0;
+    int uses = 0;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+      const int item = (int)(u / c.nrb);
+      const int* xi = a.xidx + (long long)item * a.xstride;
+      const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
+      for (int ch = 0; ch < nchunk; ++ch, ++uses) {
+        if (uses >= 2) mbar_wait(xempty + xs, xph ^ 1u);
+        double* xb = xbuf + (size_t)xs * KX * XLD;
+        const int k0 = ch * KX;
+        if (!x2) {
+          // plain gather: 16-byte cp.async copies, all in flight at once; rows past K zeroed
+          for (int e = gt; e < KX * upr; e += ST_GW * 32) {
+            const int kk = e / upr, j = 2 * (e - kk * upr), k = k0 + kk;
+            double* dst = xb + kk * XLD + j;
+            if (k < K && j + 1 < nrhs) {
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(tma_smem_addr(dst)),
+                           "l"(a.pool + (long long)__ldg(xi + k) * nrhs + j)
+                           : "memory");
+            } else {
+              dst[0] = k < K ? a.pool[(long long)__ldg(xi + k) * nrhs + j] : 0.0;
+              if (j + 1 < NRP) dst[1] = 0.0;
+            }
+          }
+          asm volatile("cp.async.wait_all;\n" ::: "memory");
+        } else {
+          for (int e0 = gt; e0 < KX * upr; e0 += 8 * ST_GW * 32) {
+            int i1[8], i2[8];
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              const int e = e0 + v * ST_GW * 32, kk = e / upr, k = k0 + kk;
+              const bool ok = e < KX * upr && k < K;
+              i1[v] = ok ? __ldg(xi + k) : -1;
+              i2[v] = ok ? __ldg(x2 + k) : -1;
+            }
+            double2 val[8];
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              const int e = e0 + v * ST_GW * 32, kk = e / upr, j = 2 * (e - kk * upr);
+              val[v] = make_double2(0.0, 0.0);
+              if (i1[v] >= 0) {
+                const double* p1 = a.pool + (long long)i1[v] * nrhs + j;
+                val[v].x = p1[0];
+                if (j + 1 < nrhs) val[v].y = p1[1];
+                if (i2[v] >= 0) {
+                  const double* p2 = a.pool + (long long)i2[v] * nrhs + j;
+                  val[v].x -= p2[0];
+                  if (j + 1 < nrhs) val[v].y -= p2[1];
+                }
+              }
+            }
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              const int e = e0 + v * ST_GW * 32, kk = e / upr, j = 2 * (e - kk * upr);
+              if (e < KX * upr) {
+                xb[kk * XLD + j] = val[v].x;
+                if (j + 1 < NRP) xb[kk * XLD + j + 1] = val[v].y;
+              }
+            }
+          }
+        }
+        mbar_arrive(xfull + xs);
+        if (++xs == 2) {
+          xs = 0;
+          xph ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumers
+  pdl_wait();  // the epilogue adds pool rows (aidx) written by the previous step
+  const int g = lane >> 2, t = lane & 3;
+  const int rg = ((g & 3) << 1) | (g >> 2);
+  int aoff[4];
+#pragma unroll
+  for (int k4 = 0; k4 < 4; ++k4) {
+    const int cc = k4 * 4 + t;
+    aoff[k4] = rg * 16 + ((((cc >> 1) ^ rg) << 1) | (cc & 1));
+  }
+  const int mt = (RB + 7) >> 3;
+  const int ntw = warp < mt ? (mt - warp + ST_NC - 1) / ST_NC : 0;
+  const bool split = a.mode2 == 3;
+  const int K2 = split ? a.K2 : 0;
+  int slot = 0, xs = 0;
+  unsigned ph = 0, xph = 0;
+  for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+    const int item = (int)(u / c.nrb), rb = (int)(u - (long long)item * c.nrb);
+    double acc[2][4][NT][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) acc[h][i][n][0] = acc[h][i][n][1] = 0.0;
+    const int* oi = a.oidx + (long long)item * a.ostride;
+    const int* ai = a.aidx ? a.aidx + (long long)item * a.ostride : nullptr;
+    const int* o2 = split ? a.o2idx + (long long)item * a.ostride : nullptr;
+    int orows[4], arows[4], wrows[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = rb * RB + (warp + i * ST_NC) * 8 + rg;
+      const bool live = i < ntw && (warp + i * ST_NC) * 8 + rg < RB && r < R;
+      orows[i] = live ? __ldg(oi + r) : -1;
+      arows[i] = (live && ai) ? __ldg(ai + r) : -1;
+      wrows[i] = (live && o2) ? __ldg(o2 + r) : -1;
+    }
+    for (int ch = 0; ch < nchunk; ++ch) {
+      mbar_wait(xfull + xs, xph);
+      const double* xc = xbuf + (size_t)xs * KX * XLD;
+      const int js = ch * spc, je = min(nslab, js + spc);
+      for (int j = js; j < je; ++j) {
+        mbar_wait(full + slot, ph);
+        const double* slab = reinterpret_cast<const double*>(base + (size_t)slot * c.sb_bytes);
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+          const int kl = (j - js) * 16 + k4 * 4;  // column within the chunk
+          const int h = split ? (ch * KX + kl < K2 ? 0 : 1) : (k4 & 1);
+          double bv[NT];
+#pragma unroll
+          for (int n = 0; n < NT; ++n) bv[n] = xc[(kl + t) * XLD + n * 8 + g];
+          // the tile count is warp-uniform: one branch-free body per count (a guarded DMMA would
+          // still occupy the tensor pipe)
+          switch (ntw) {
+            case 1: stream_k4<1, NT>(acc, h, slab, warp, aoff[k4], bv); break;
+            case 2: stream_k4<2, NT>(acc, h, slab, warp, aoff[k4], bv); break;
+            case 3: stream_k4<3, NT>(acc, h, slab, warp, aoff[k4], bv); break;
+            case 4: stream_k4<4, NT>(acc, h, slab, warp, aoff[k4], bv); break;
+            default: break;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + slot);
+        if (++slot == ns) {
+          slot = 0;
+          ph ^= 1u;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(xempty + xs);
+      if (++xs == 2) {
+        xs = 0;
+        xph ^= 1u;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (orows[i] < 0) continue;
+      const long long orow = (long long)orows[i] * nrhs;
+#pragma unroll
+      for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int j = n * 8 + 2 * t + hh;
+          if (j < nrhs) {
+            double v = acc[0][i][n][hh] + acc[1][i][n][hh];
+            if (arows[i] >= 0) v += a.pool[(long long)arows[i] * nrhs + j];
+            if (wrows[i] >= 0) a.pool[(long long)wrows[i] * nrhs + j] = acc[0][i][n][hh];
+            a.pool[orow + j] = v;
+          }
+        }
+    }
+  }
+}
+
+// Returns true when the step was launched on the streaming kernel.
+bool launch_gemv_stream(const GemvArgs& a, cudaStream_t s) {
+  static const int on = [] {
+    const char* e = getenv("HPS_STREAM");
+    return e ? atoi(e) : 1;
+  }();
+  static const long long min_bytes = [] {  // HPS_STREAM_MIN_KB: smallest item routed here
+    const char* e = getenv("HPS_STREAM_MIN_KB");
+    return 1024LL * (e ? atoll(e) : 48);
+  }();
+  if (!on || a.nrhs <= 2 || a.nrhs > 16 || a.A.ptrs || (a.mode2 != 0 && a.mode2 != 3)) return false;
+  if (a.R < 32 || a.K < 64 || 8LL * a.R * a.K < min_bytes) return false;
+  if (a.mode2 == 3 && (a.K2 % 4 != 0 || a.kparts > 1)) return false;
+  const int kp = a.kparts > 1 ? a.kparts : 1;
+  const long long nops = a.nitems / kp;  // operator items
+  if (a.A.stride != (long long)a.R * a.A.ld || (a.A.ld * 8) % 16 != 0 || (long long)kp * a.K > a.A.ld) return false;
+  const double* gbase = a.A.base + a.A.off;
+  if (reinterpret_cast<uintptr_t>(gbase) % 16 != 0) return false;
+  if (a.nrhs % 2 == 0 && reinterpret_cast<uintptr_t>(a.pool) % 16 != 0) return false;
+  auto enc = encode_fn();
+  if (!enc) return false;
+
+  StreamCfg c{};
+  // row blocks: the whole item when it has <= 256 rows, else equal blocks rounded up to m-tiles
+  const int nb = (a.R + 255) / 256;
+  c.RB = nb == 1 ? a.R : (((a.R + nb - 1) / nb) + 7) & ~7;
+  c.nrb = (a.R + c.RB - 1) / c.RB;
+  c.KX = 128;
+  c.sb_bytes = ((c.RB * 128 + 1023) / 1024) * 1024;
+  const int nrp = a.nrhs <= 8 ? 8 : 16;
+  const size_t xbytes = 2 * sizeof(double) * (size_t)c.KX * (nrp + 4);
+  const size_t budget = 220 * 1024;
+  c.ns = 8;
+  while (c.ns > 2 && 1024 + (size_t)c.ns * c.sb_bytes + xbytes + 16 * (c.ns + 2) > budget) --c.ns;
+  const size_t smem = 1024 + (size_t)c.ns * c.sb_bytes + xbytes + 16 * (size_t)(c.ns + 2);
+  if (smem > budget) return false;
+
+  CUtensorMap tm;
+  const cuuint64_t dims[2] = {(cuuint64_t)a.A.ld, (cuuint64_t)(nops * a.R)};
+  const cuuint64_t strides[1] = {(cuuint64_t)a.A.ld * 8};
+  const cuuint32_t box[2] = {16, (cuuint32_t)c.RB};
+  const cuuint32_t estr[2] = {1, 1};
+  if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(gbase), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long units = (long long)a.nitems * c.nrb;
+  const int grid = (int)(units < sms ? units : sms);
+  using KFn = void (*)(const CUtensorMap, GemvArgs, StreamCfg);
+  const KFn k = nrp == 16 ? gemv_stream_kernel<16> : gemv_stream_kernel<8>;
+  static bool configured[2] = {};
+  if (!configured[nrp == 16]) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
+    configured[nrp == 16] = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(ST_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, tm, a, c) == cudaSuccess;
 }
 
 }  // namespace hps

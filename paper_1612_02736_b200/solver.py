@@ -861,44 +861,55 @@ class FactorizedSolver:
         scratch = [lay["rows"]]
 
         def split(spec):
-            if spec["mode2"] not in (0, 3) or spec["K"] < 512 or "patch" in spec:
+            if spec["mode2"] not in (0, 3) or "patch" in spec:
                 # (economy-mode leaf steps take their operator base per solve: never split)
                 return [spec]
-            K = spec["K"]
-            # the single-launch sweep program stages each step's x in 48 KB of shared memory
-            must = nrhs <= 2 and K * 8 * nrhs > 40 * 1024
-            if not must and nrhs <= 2 and 8 * spec["nitems"] * spec["R"] * K < _SPLIT_BYTES:
-                return [spec]  # single-RHS: the extra reduction step costs more than it saves
-            rows_min = 16 if nrhs > 2 else 8
-            ctas = spec["nitems"] * -(-spec["R"] // rows_min)
-            if ctas >= _SPLIT_CTAS and not must:
-                return [spec]
-            want = max(min(-(-_SPLIT_CTAS // ctas), K // 128), -(-K * 8 * nrhs // (40 * 1024)) if must else 1)
-            if spec["mode2"] == 3:
-                # every partial lies on one side of the w3 boundary K2: kc divides K2 and K - K2
-                K2 = spec["K2"]
-                ok = [d for d in range(2, K + 1) if K % d == 0 and K2 % (K // d) == 0]
-                if must:
-                    ok = [d for d in ok if (K // d) * 8 * nrhs <= 40 * 1024]
-                below = [d for d in ok if d <= max(want, 1)]
-                ns = max(below) if below else (min(ok) if ok else 1)
+            K, R, n = spec["K"], spec["R"], spec["nitems"]
+            K2 = spec["K2"] if spec["mode2"] == 3 else 0
+            if nrhs > 2:
+                # multi-RHS: the TMA-streamed kernel (launch_gemv_stream) takes units of one item x
+                # <= 256 rows; split K until the step has ~2 units per SM (parts of >= 128 columns)
+                if K < 256 or R < 64 or 8 * R * K < 48 * 1024:
+                    return [spec]
+                units = n * -(-R // 256)
+                if units >= 2 * 148:
+                    return [spec]
+                want = -(-2 * 148 // units)
+                ok = [d for d in range(2, K // 128 + 1) if K % d == 0 and (not K2 or K2 % (K // d) == 0)]
+                if not ok:
+                    return [spec]
+                above = [d for d in ok if d >= want]
+                ns = min(above) if above else max(ok)
             else:
-                ns = min([d for d in range(want, K + 1) if K % d == 0] or [1]) if must else \
-                    max([d for d in range(1, want + 1) if K % d == 0] or [1])
+                if K < 512:
+                    return [spec]
+                # the single-launch sweep program stages each step's x in 48 KB of shared memory
+                must = K * 8 * nrhs > 40 * 1024
+                if not must and 8 * n * R * K < _SPLIT_BYTES:
+                    return [spec]  # single-RHS: the extra reduction step costs more than it saves
+                ctas = n * -(-R // 8)
+                if ctas >= _SPLIT_CTAS and not must:
+                    return [spec]
+                want = max(min(-(-_SPLIT_CTAS // ctas), K // 128), -(-K * 8 * nrhs // (40 * 1024)) if must else 1)
+                if spec["mode2"] == 3:
+                    # every partial lies on one side of the w3 boundary K2: kc divides K2 and K - K2
+                    ok = [d for d in range(2, K + 1) if K % d == 0 and K2 % (K // d) == 0]
+                    if must:
+                        ok = [d for d in ok if (K // d) * 8 * nrhs <= 40 * 1024]
+                    below = [d for d in ok if d <= max(want, 1)]
+                    ns = max(below) if below else (min(ok) if ok else 1)
+                else:
+                    ns = min([d for d in range(want, K + 1) if K % d == 0] or [1]) if must else \
+                        max([d for d in range(1, want + 1) if K % d == 0] or [1])
             if ns <= 1:
                 return [spec]
             kc = K // ns
-            A, n, R = spec["A"], spec["nitems"], spec["R"]
-            base = A.base if A.base else 0
-            ptrs = np.array([base + 8 * (i * A.stride + A.off + s * kc) for i in range(n) for s in range(ns)],
-                            dtype=np.int64)
-            ptr_t = torch.as_tensor(ptrs, device=self.device)
-            keep.append(ptr_t)
             scr0 = scratch[0]
             scratch[0] += n * ns * R
             t = np.arange(n * ns)
+            # split-K parts: item i * ns + s = column block s of operator item i (ABI kparts)
             part = dict(spec)
-            part.update(nitems=n * ns, K=kc, A=_ext.MatBatch(0, 0, ptr_t.data_ptr(), A.ld, 0),
+            part.update(nitems=n * ns, K=kc, kparts=ns,
                         xidx=spec["xidx"].reshape(n, ns, kc).reshape(n * ns, kc),
                         x2idx=None if spec["x2idx"] is None else spec["x2idx"].reshape(n * ns, kc),
                         aidx=None, oidx=scr0 + t[:, None] * R + np.arange(R)[None, :],
@@ -963,7 +974,7 @@ class FactorizedSolver:
             A2 = spec["A2"] if spec["A2"] is not None else _ext.MatBatch()
             return _ext.GemvBatch(spec["nitems"], spec["R"], spec["K"], nrhs, spec["A"], pool.data_ptr(),
                                   xi.data_ptr(), _ext.ptr(x2), _ext.ptr(ai), oi.data_ptr(), spec["mode2"],
-                                  spec["R2"], spec["K2"], A2, _ext.ptr(a2), _ext.ptr(o2))
+                                  spec["R2"], spec["K2"], A2, _ext.ptr(a2), _ext.ptr(o2), spec.get("kparts", 0))
 
         patches = [(k, i, s_["patch"]) for k, lst in (("up", up), ("down", down), ("down_w", down_w))
                    for i, s_ in enumerate(lst) if "patch" in s_]
