@@ -1100,6 +1100,7 @@ int launch_gemv_gather(const GemvArgs& a, cudaStream_t s) {
     const bool ok = a.nrhs == 1 ? launch_sweep<1>(a, s) : launch_sweep<2>(a, s);
     if (ok) return cudaGetLastError() == cudaSuccess ? 0 : 2;
   }
+  if (a.nrhs > 2 && a.mode2 == 1 && launch_gemv_stream(a, s)) return cudaGetLastError() == cudaSuccess ? 0 : 2;
   if (a.nrhs > 2 && launch_gemv_tma(a, s)) return cudaGetLastError() == cudaSuccess ? 0 : 2;
   if (a.nrhs > 2 && launch_gemv_stream(a, s)) return cudaGetLastError() == cudaSuccess ? 0 : 2;
   if (a.nrhs > 2 && a.nrhs <= 16 && a.R > 1 && !a.A.ptrs) {

@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "hps_common.cuh"
@@ -461,34 +462,49 @@ bool launch_gemv_tma(const GemvArgs& a, cudaStream_t s) {
 //   warps 9..10  gather:   x chunks of KX columns (x = pool[xidx] - pool[x2idx], zero padded)
 //                          -> a double-buffered smem ring, with the x2 difference applied
 //   warps 0..7   DMMA consumers, 4 m-tiles of 8 rows each (tile w, w+8, w+16, w+24)
-// mode2 = 3 (parent downward [X | S][d; u_ext]): columns < K2 accumulate into one accumulator
-// set, the rest into the other; w3 = the first, u3 = their sum. Otherwise the two sets take
-// alternating k4 steps (two independent DMMA chains per tile).
+// The two accumulator sets take alternating k4 steps (two independent DMMA chains per tile);
+// mode2 = 3 (parent downward [X | S][d; u_ext]) stores their sum at column K2 as w3 = X d.
 // Why: the register-streaming gemv_dmma_kernel kept ~16 KB per SM in flight and ran the config-5
 // top levels at 0.2-2.5 TB/s (root downward partials: 147 MB in 123 us).
 constexpr int ST_NC = 8, ST_GW = 4, ST_THREADS = 32 * (ST_NC + 1 + ST_GW);
 
 struct StreamCfg {
   int RB, nrb, KX, ns, sb_bytes;
+  int ld2;  // mode2 = 1: padded row length of the shared tail operator A2 staged in smem
+  int nxb;  // x chunk buffers in the gather ring (2..4)
 };
 
-// one k4 step of T m-tiles into accumulator set h
-template <int T, int NT>
-__device__ __forceinline__ void stream_k4(double (&acc)[2][4][NT][2], int h, const double* slab, int warp, int aoff,
-                                          const double (&bv)[NT]) {
-  double av[T];
+// One 16-column slab for T m-tiles: 4 k4 steps into the two accumulator sets by parity. ksnap:
+// chunk-local column where w3 = the partial sum is taken (mode2 = 3), else negative.
+template <int T, int NT, int XLD>
+__device__ __forceinline__ void stream_slab(double (&acc)[2][4][NT][2], const double* slab, const double* xc, int kl0,
+                                            int ksnap, const int (&aoff)[4], int warp, int g, int t,
+                                            const int (&wrows)[4], double* pool, int nrhs) {
 #pragma unroll
-  for (int i = 0; i < T; ++i) av[i] = slab[(warp + i * ST_NC) * 128 + aoff];
-  if (h == 0) {
+  for (int k4 = 0; k4 < 4; ++k4) {
+    const int kl = kl0 + k4 * 4;
+    if (kl == ksnap) {
+      // w3 = the partial sum over [0, K2) is final here: stored straight to its pool rows
+#pragma unroll
+      for (int i = 0; i < T; ++i)
+        if (wrows[i] >= 0)
+#pragma unroll
+          for (int n = 0; n < NT; ++n)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const int j = n * 8 + 2 * t + hh;
+              if (j < nrhs) pool[(long long)wrows[i] * nrhs + j] = acc[0][i][n][hh] + acc[1][i][n][hh];
+            }
+    }
+    double bv[NT], av[T];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) bv[n] = xc[(kl + t) * XLD + n * 8 + g];
+#pragma unroll
+    for (int i = 0; i < T; ++i) av[i] = slab[(warp + i * ST_NC) * 128 + aoff[k4]];
 #pragma unroll
     for (int i = 0; i < T; ++i)
 #pragma unroll
-      for (int n = 0; n < NT; ++n) dmma_nv(acc[0][i][n][0], acc[0][i][n][1], av[i], bv[n]);
-  } else {
-#pragma unroll
-    for (int i = 0; i < T; ++i)
-#pragma unroll
-      for (int n = 0; n < NT; ++n) dmma_nv(acc[1][i][n][0], acc[1][i][n][1], av[i], bv[n]);
+      for (int n = 0; n < NT; ++n) dmma_nv(acc[k4 & 1][i][n][0], acc[k4 & 1][i][n][1], av[i], bv[n]);
   }
 }
 
@@ -504,17 +520,18 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
   const int nslab = (K + 15) >> 4, nchunk = (K + KX - 1) / KX, spc = KX >> 4;
   const long long units = (long long)a.nitems * c.nrb;
   double* xbuf = reinterpret_cast<double*>(base + (size_t)ns * c.sb_bytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + 2 * (size_t)KX * XLD);
+  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + (size_t)c.nxb * KX * XLD);
   uint64_t* empty = full + ns;
   uint64_t* xfull = empty + ns;
-  uint64_t* xempty = xfull + 2;
+  uint64_t* xempty = xfull + 4;
+  double* a2s = reinterpret_cast<double*>(xempty + 4);  // mode2 = 1: R2 x ld2
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int i = 0; i < ns; ++i) {
       mbar_init(full + i, 1);
       mbar_init(empty + i, ST_NC);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < c.nxb; ++i) {
       mbar_init(xfull + i, ST_GW * 32);
       mbar_init(xempty + i, ST_NC);
     }
@@ -561,21 +578,40 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
       const int* xi = a.xidx + (long long)item * a.xstride;
       const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
       for (int ch = 0; ch < nchunk; ++ch, ++uses) {
-        if (uses >= 2) mbar_wait(xempty + xs, xph ^ 1u);
+        if (uses >= c.nxb) mbar_wait(xempty + xs, xph ^ 1u);
         double* xb = xbuf + (size_t)xs * KX * XLD;
         const int k0 = ch * KX;
         if (!x2) {
-          // plain gather: 16-byte cp.async copies, all in flight at once; rows past K zeroed
-          for (int e = gt; e < KX * upr; e += ST_GW * 32) {
-            const int kk = e / upr, j = 2 * (e - kk * upr), k = k0 + kk;
-            double* dst = xb + kk * XLD + j;
-            if (k < K && j + 1 < nrhs) {
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(tma_smem_addr(dst)),
-                           "l"(a.pool + (long long)__ldg(xi + k) * nrhs + j)
-                           : "memory");
-            } else {
-              dst[0] = k < K ? a.pool[(long long)__ldg(xi + k) * nrhs + j] : 0.0;
-              if (j + 1 < NRP) dst[1] = 0.0;
+          // plain gather: 16-byte cp.async copies; the indices of 8 units are loaded together so
+          // their latencies overlap, then all copies go out at once; rows past K are zeroed
+          for (int e0 = gt; e0 < KX * upr; e0 += 8 * ST_GW * 32) {
+            int i1[8];
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              const int e = e0 + v * ST_GW * 32, kk = e / upr, k = k0 + kk;
+              i1[v] = (e < KX * upr && k < K) ? __ldg(xi + k) : -1;
+            }
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              const int e = e0 + v * ST_GW * 32, kk = e / upr, j = 2 * (e - kk * upr);
+              if (e >= KX * upr) continue;
+              double* dst = xb + kk * XLD + j;
+              if (i1[v] >= 0 && j + 1 < nrhs && !(nrhs & 1)) {  // 16-byte copies need an even row length
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(tma_smem_addr(dst)),
+                             "l"(a.pool + (long long)i1[v] * nrhs + j)
+                             : "memory");
+              } else if (i1[v] >= 0) {
+                const double* src = a.pool + (long long)i1[v] * nrhs + j;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(tma_smem_addr(dst)), "l"(src) : "memory");
+                if (j + 1 < nrhs)
+                  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(tma_smem_addr(dst + 1)), "l"(src + 1)
+                               : "memory");
+                else if (j + 1 < NRP)
+                  dst[1] = 0.0;
+              } else {
+                dst[0] = 0.0;
+                if (j + 1 < NRP) dst[1] = 0.0;
+              }
             }
           }
           asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -616,7 +652,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
           }
         }
         mbar_arrive(xfull + xs);
-        if (++xs == 2) {
+        if (++xs == c.nxb) {
           xs = 0;
           xph ^= 1u;
         }
@@ -626,6 +662,17 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
   }
 
   // ---- consumers
+  const bool tail = a.mode2 == 1;
+  if (tail) {
+    // the level's shared tail operator (leaf down: the lift L) -> smem once per CTA (static data)
+    const double* A2 = a.A2.get(0);
+    const int r2p = (a.R2 + 7) & ~7;  // whole 8-row tiles (rows past R2 zero)
+    for (int e = tid; e < r2p * c.ld2; e += ST_NC * 32) {
+      const int r = e / c.ld2, k = e - r * c.ld2;
+      a2s[e] = (r < a.R2 && k < a.K2) ? __ldg(A2 + (long long)r * a.A2.ld + k) : 0.0;
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"n"(ST_NC * 32) : "memory");
+  }
   pdl_wait();  // the epilogue adds pool rows (aidx) written by the previous step
   const int g = lane >> 2, t = lane & 3;
   const int rg = ((g & 3) << 1) | (g >> 2);
@@ -669,22 +716,15 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
       for (int j = js; j < je; ++j) {
         mbar_wait(full + slot, ph);
         const double* slab = reinterpret_cast<const double*>(base + (size_t)slot * c.sb_bytes);
-#pragma unroll
-        for (int k4 = 0; k4 < 4; ++k4) {
-          const int kl = (j - js) * 16 + k4 * 4;  // column within the chunk
-          const int h = split ? (ch * KX + kl < K2 ? 0 : 1) : (k4 & 1);
-          double bv[NT];
-#pragma unroll
-          for (int n = 0; n < NT; ++n) bv[n] = xc[(kl + t) * XLD + n * 8 + g];
-          // the tile count is warp-uniform: one branch-free body per count (a guarded DMMA would
-          // still occupy the tensor pipe)
-          switch (ntw) {
-            case 1: stream_k4<1, NT>(acc, h, slab, warp, aoff[k4], bv); break;
-            case 2: stream_k4<2, NT>(acc, h, slab, warp, aoff[k4], bv); break;
-            case 3: stream_k4<3, NT>(acc, h, slab, warp, aoff[k4], bv); break;
-            case 4: stream_k4<4, NT>(acc, h, slab, warp, aoff[k4], bv); break;
-            default: break;
-          }
+        // the tile count is warp-uniform: one branch-free slab body per count (a guarded DMMA
+        // would still occupy the tensor pipe)
+        const int kl0 = (j - js) * 16, ksnap = split ? K2 - ch * KX : -1;
+        switch (ntw) {
+          case 1: stream_slab<1, NT, XLD>(acc, slab, xc, kl0, ksnap, aoff, warp, g, t, wrows, a.pool, nrhs); break;
+          case 2: stream_slab<2, NT, XLD>(acc, slab, xc, kl0, ksnap, aoff, warp, g, t, wrows, a.pool, nrhs); break;
+          case 3: stream_slab<3, NT, XLD>(acc, slab, xc, kl0, ksnap, aoff, warp, g, t, wrows, a.pool, nrhs); break;
+          case 4: stream_slab<4, NT, XLD>(acc, slab, xc, kl0, ksnap, aoff, warp, g, t, wrows, a.pool, nrhs); break;
+          default: break;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + slot);
@@ -693,9 +733,34 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
           ph ^= 1u;
         }
       }
+      if (tail && ch == nchunk - 1 && warp * 8 < a.R2) {
+        // tail y2 = A2 x[K-K2, K) (leaf down: exterior rows u_ce = L u_ge) from the last x chunk;
+        // one 8-row tile per warp
+        const int xo = (K - a.K2) - ch * KX;
+        double c2[NT][2];
+#pragma unroll
+        for (int n = 0; n < NT; ++n) c2[n][0] = c2[n][1] = 0.0;
+        const double* arow = a2s + (size_t)(warp * 8 + g) * c.ld2;
+        for (int k = 0; k < a.K2; k += 4) {
+          const double av = arow[k + t];
+#pragma unroll
+          for (int n = 0; n < NT; ++n) dmma_nv(c2[n][0], c2[n][1], av, xc[(xo + k + t) * XLD + n * 8 + g]);
+        }
+        const int ra = warp * 8 + g;
+        if (ra < a.R2) {
+          const long long orow = (long long)__ldg(a.o2idx + (long long)item * a.R2 + ra) * nrhs;
+#pragma unroll
+          for (int n = 0; n < NT; ++n)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const int j = n * 8 + 2 * t + hh;
+              if (j < nrhs) a.pool[orow + j] = c2[n][hh];
+            }
+        }
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(xempty + xs);
-      if (++xs == 2) {
+      if (++xs == c.nxb) {
         xs = 0;
         xph ^= 1u;
       }
@@ -712,7 +777,6 @@ __global__ void __launch_bounds__(ST_THREADS, 1)
           if (j < nrhs) {
             double v = acc[0][i][n][hh] + acc[1][i][n][hh];
             if (arows[i] >= 0) v += a.pool[(long long)arows[i] * nrhs + j];
-            if (wrows[i] >= 0) a.pool[(long long)wrows[i] * nrhs + j] = acc[0][i][n][hh];
             a.pool[orow + j] = v;
           }
         }
@@ -730,9 +794,19 @@ bool launch_gemv_stream(const GemvArgs& a, cudaStream_t s) {
     const char* e = getenv("HPS_STREAM_MIN_KB");
     return 1024LL * (e ? atoll(e) : 48);
   }();
-  if (!on || a.nrhs <= 2 || a.nrhs > 16 || a.A.ptrs || (a.mode2 != 0 && a.mode2 != 3)) return false;
+  if (!on || a.nrhs <= 2 || a.nrhs > 16 || a.A.ptrs || a.mode2 == 2) return false;
   if (a.R < 32 || a.K < 64 || 8LL * a.R * a.K < min_bytes) return false;
   if (a.mode2 == 3 && (a.K2 % 4 != 0 || a.kparts > 1)) return false;
+  // mode2 = 1 (tail): a level-shared A2, at most one 8-row tile per consumer warp, K2 % 4 == 0,
+  // and the tail's x columns inside the last 128-column x chunk
+  if (a.mode2 == 1 && (a.A2.stride != 0 || a.A2.ptrs || a.a2idx || a.R2 > 8 * ST_NC || a.K2 % 4 != 0 ||
+                       a.K2 > 128 || (a.K - a.K2) < ((a.K + 127) / 128 - 1) * 128 || a.kparts > 1))
+    return false;
+  static const int leaf_on = [] {  // HPS_STREAM_LEAF=1: also the leaf downward step (mode2 = 1)
+    const char* e = getenv("HPS_STREAM_LEAF");
+    return e ? atoi(e) : 0;
+  }();
+  if (a.mode2 == 1 && !leaf_on) return false;
   const int kp = a.kparts > 1 ? a.kparts : 1;
   const long long nops = a.nitems / kp;  // operator items
   if (a.A.stride != (long long)a.R * a.A.ld || (a.A.ld * 8) % 16 != 0 || (long long)kp * a.K > a.A.ld) return false;
@@ -750,11 +824,15 @@ bool launch_gemv_stream(const GemvArgs& a, cudaStream_t s) {
   c.KX = 128;
   c.sb_bytes = ((c.RB * 128 + 1023) / 1024) * 1024;
   const int nrp = a.nrhs <= 8 ? 8 : 16;
-  const size_t xbytes = 2 * sizeof(double) * (size_t)c.KX * (nrp + 4);
+  // x chunk ring: enough buffers for the gather to run two units ahead of the consumers
+  c.nxb = std::min(4, std::max(2, 2 * ((a.K + c.KX - 1) / c.KX)));
+  const size_t xbytes = (size_t)c.nxb * sizeof(double) * (size_t)c.KX * (nrp + 4);
   const size_t budget = 220 * 1024;
+  c.ld2 = a.mode2 == 1 ? ((a.K2 + 11) & ~15) + 4 : 0;  // == 4 mod 16: conflict-free fragments
+  const size_t a2bytes = a.mode2 == 1 ? sizeof(double) * (size_t)((a.R2 + 7) & ~7) * c.ld2 : 0;
   c.ns = 8;
-  while (c.ns > 2 && 1024 + (size_t)c.ns * c.sb_bytes + xbytes + 16 * (c.ns + 2) > budget) --c.ns;
-  const size_t smem = 1024 + (size_t)c.ns * c.sb_bytes + xbytes + 16 * (size_t)(c.ns + 2);
+  while (c.ns > 2 && 1024 + (size_t)c.ns * c.sb_bytes + xbytes + 16 * (c.ns + 8) + a2bytes > budget) --c.ns;
+  const size_t smem = 1024 + (size_t)c.ns * c.sb_bytes + xbytes + 16 * (size_t)(c.ns + 8) + a2bytes;
   if (smem > budget) return false;
 
   CUtensorMap tm;

@@ -664,6 +664,97 @@ class FactorizedSolver:
             return res
 
     # -- sweep program ----------------------------------------------------------------------
+    MERGE_BYTES = int(os.environ.get("HPS_MERGE_BYTES", str(16 << 20)))
+
+    def _merge_levels(self, steps, gemv, zero_row, trash_row, keep):
+        """Batch the small parent steps of one tree level into one padded launch per role.
+
+        Shape groups of one depth (refined meshes: every wrapped parent is its own group) are
+        independent, so their steps can share a launch once each item is zero-padded to the
+        level's largest (R, K): padded operator columns meet x rows gathered from a pool row that
+        is always zero, padded output rows go to a scratch row nobody reads. Roles keep their
+        order inside a level (upward: parent steps, then the wrap interpolations that read their
+        output; downward: the fine-edge interpolations, then the parent steps). Only levels whose
+        padded operators stay under MERGE_BYTES are merged: this targets latency-bound meshes
+        (config 4: 84 parent groups over 22 levels), not the large uniform levels."""
+        out, i = [], 0
+        while i < len(steps):
+            mk = steps[i].get("mk")
+            if mk is None:
+                out.append(steps[i])
+                i += 1
+                continue
+            j = i
+            while j < len(steps) and steps[j].get("mk") is not None and steps[j]["mk"][0] == mk[0]:
+                j += 1
+            run = steps[i:j]
+            roles = []
+            for st in run:
+                if st["mk"][1] not in roles:
+                    roles.append(st["mk"][1])
+            for role in sorted(roles, key=lambda r_: {"wrapu": 0, "par": 1, "wrapq": 2}[r_]):
+                grp = [st for st in run if st["mk"][1] == role]
+                by_mode = {}
+                for st in grp:
+                    by_mode.setdefault(st["mode2"], []).append(st)
+                for mode2, sts in by_mode.items():
+                    if len(sts) >= 2 and self._padded_bytes(sts) <= self.MERGE_BYTES:
+                        out.append(self._merge_run(sts, gemv, zero_row, trash_row, keep))
+                    else:
+                        out.extend(sts)
+            i = j
+        return out
+
+    @staticmethod
+    def _padded_bytes(sts):
+        n = sum(st["nitems"] for st in sts)
+        R = max(st["R"] for st in sts)
+        if sts[0]["mode2"] == 3:
+            K = max(st["K2"] for st in sts) + max(st["K"] - st["K2"] for st in sts)
+        else:
+            K = max(st["K"] for st in sts)
+        return 8 * n * R * K
+
+    def _merge_run(self, sts, gemv, zero_row, trash_row, keep):
+        split3 = sts[0]["mode2"] == 3
+        n = sum(st["nitems"] for st in sts)
+        R = max(st["R"] for st in sts)
+        K2 = max(st["K2"] for st in sts) if split3 else 0
+        K = K2 + max(st["K"] - st["K2"] for st in sts) if split3 else max(st["K"] for st in sts)
+        A = _op_empty((n, R, K), self.device)
+        A.zero_()
+        x = np.full((n, K), zero_row, dtype=np.int64)
+        x2 = np.full((n, K), -1, dtype=np.int64)
+        o = np.full((n, R), trash_row, dtype=np.int64)
+        o2 = np.full((n, R), trash_row, dtype=np.int64) if split3 else None
+        has_a = any(st["aidx"] is not None for st in sts)
+        a = np.full((n, R), zero_row, dtype=np.int64) if has_a else None
+        has_x2 = any(st["x2idx"] is not None for st in sts)
+        off = 0
+        for st in sts:
+            ni, Ri, Ki = st["nitems"], st["R"], st["K"]
+            At = st["At"]
+            sl = slice(off, off + ni)
+            if split3:
+                k2 = st["K2"]
+                A[sl, :Ri, :k2] = At[:, :, :k2]
+                A[sl, :Ri, K2:K2 + Ki - k2] = At[:, :, k2:]
+                cols = np.concatenate([np.arange(k2), K2 + np.arange(Ki - k2)])
+                o2[sl, :Ri] = st["o2idx"]
+            else:
+                A[sl, :Ri, :Ki] = At
+                cols = np.arange(Ki)
+            x[sl, cols] = st["xidx"]
+            if st["x2idx"] is not None:
+                x2[sl, cols] = st["x2idx"]
+            o[sl, :Ri] = st["oidx"]
+            if st["aidx"] is not None:
+                a[sl, :Ri] = st["aidx"]
+            off += ni
+        keep.append(A)
+        return gemv(n, R, K, _ext.mat(A, R * K, K), x, o, x2idx=x2 if has_x2 else None, aidx=a,
+                    mode2=3 if split3 else 0, R2=R if split3 else 0, K2=K2, o2idx=o2)
+
     use_graphs = True
 
     def _steps(self, prog, phase="full", leaves_down=True):
@@ -748,12 +839,14 @@ class FactorizedSolver:
         keep = []
 
         def gemv(nitems, R, K, A, xidx, oidx, x2idx=None, aidx=None, mode2=0, R2=0, K2=0, A2=None,
-                 o2idx=None, a2idx=None):
+                 o2idx=None, a2idx=None, mk=None, At=None):
+            # mk = (depth, role), At = (nitems, R, K) tensor view of the operator: lets
+            # _merge_levels batch the small steps of one tree level into one padded launch
             return dict(nitems=nitems, R=R, K=K, A=A, xidx=np.asarray(xidx), oidx=np.asarray(oidx),
                         x2idx=None if x2idx is None else np.asarray(x2idx),
                         aidx=None if aidx is None else np.asarray(aidx), mode2=mode2, R2=R2, K2=K2, A2=A2,
                         o2idx=None if o2idx is None else np.asarray(o2idx),
-                        a2idx=None if a2idx is None else np.asarray(a2idx))
+                        a2idx=None if a2idx is None else np.asarray(a2idx), mk=mk, At=At)
 
         up, down = [], []
         p, q = self.p, self.q
@@ -790,16 +883,21 @@ class FactorizedSolver:
             nI = len(grp.ids)
             xw, x2w, ow = np.stack(xw), np.stack(x2w), np.stack(ow)
             dgather[id(grp)] = (xw, x2w, ow)
-            up.append(gemv(nI, e, m3, _ext.mat(grp.y, e * m3, m3), xw, np.stack(oh), x2idx=x2w, aidx=np.stack(ah)))
+            d = grp.depth
+            up.append(gemv(nI, e, m3, _ext.mat(grp.y, e * m3, m3), xw, np.stack(oh), x2idx=x2w, aidx=np.stack(ah),
+                           mk=(d, "par"), At=grp.y))
             if grp.wrap is not None:
                 ldx = m3 + grp.wrap["ec"]
-                wonly.append(gemv(1, m3, m3, _ext.mat(grp.wrap["xsw"], 0, ldx), xw, ow, x2idx=x2w))
+                wonly.append(gemv(1, m3, m3, _ext.mat(grp.wrap["xsw"], 0, ldx), xw, ow, x2idx=x2w,
+                                  mk=(d, "par"), At=grp.wrap["xsw"][None, :, :m3]))
                 nid = grp.ids[0]
                 ec = grp.wrap["ec"]
                 up.append(gemv(1, ec, e, _ext.mat(grp.wrap["qd_dev"], 0, e),
-                               (lay["hpre"][nid] + np.arange(e))[None], (hslot[nid] + np.arange(ec))[None]))
+                               (lay["hpre"][nid] + np.arange(e))[None], (hslot[nid] + np.arange(ec))[None],
+                               mk=(d, "wrapq"), At=grp.wrap["qd_dev"][None]))
             else:
-                wonly.append(gemv(nI, m3, m3, _ext.mat(grp.xs, m3 * (m3 + e), m3 + e), xw, ow, x2idx=x2w))
+                wonly.append(gemv(nI, m3, m3, _ext.mat(grp.xs, m3 * (m3 + e), m3 + e), xw, ow, x2idx=x2w,
+                                  mk=(d, "par"), At=grp.xs[:, :, :m3]))
         # downward: parents root first: u[j3] = [X | S][d; u_ext] = w3 + S u_ext, and w[j3] = w3 as
         # the partial sum over the first m3 columns (solver.py:284,329-335); x2idx = -1 on the S
         # part (no difference operand)
@@ -812,18 +910,21 @@ class FactorizedSolver:
                 ec = grp.wrap["ec"]
                 ext = lay["U"] + en.ext
                 down.append(gemv(1, e, ec, _ext.mat(grp.wrap["pu_dev"], 0, ec), ext[None],
-                                 (lay["U"] + en.wrap.fine)[None]))
+                                 (lay["U"] + en.wrap.fine)[None], mk=(grp.depth, "wrapu"),
+                                 At=grp.wrap["pu_dev"][None]))
                 xi = np.concatenate([xw, ext[None]], axis=1)
                 x2 = np.concatenate([x2w, np.full((1, ec), -1)], axis=1)
                 down.append(gemv(1, m3, m3 + ec, _ext.mat(grp.wrap["xsw"], 0, m3 + ec), xi,
-                                 (lay["U"] + en.j3)[None], x2idx=x2, mode2=3, R2=m3, K2=m3, o2idx=ow))
+                                 (lay["U"] + en.j3)[None], x2idx=x2, mode2=3, R2=m3, K2=m3, o2idx=ow,
+                                 mk=(grp.depth, "par"), At=grp.wrap["xsw"][None]))
                 continue
             ext = np.stack([lay["U"] + plan.node[n].ext_mergeorder for n in grp.ids])
             xi = np.concatenate([xw, ext], axis=1)
             x2 = np.concatenate([x2w, np.full(ext.shape, -1)], axis=1)
             j3 = np.stack([plan.node[n].j3 for n in grp.ids])
             down.append(gemv(len(grp.ids), m3, m3 + e, _ext.mat(grp.xs, m3 * (m3 + e), m3 + e), xi,
-                             lay["U"] + j3, x2idx=x2, mode2=3, R2=m3, K2=m3, o2idx=ow))
+                             lay["U"] + j3, x2idx=x2, mode2=3, R2=m3, K2=m3, o2idx=ow,
+                             mk=(grp.depth, "par"), At=grp.xs))
         # downward pass from a stored w (downward_pass): u[j3] = S u_ext + w[j3] with S the last
         # e (e_c) columns of [X | S] (solver.py:329-335)
         down_w = []
@@ -835,14 +936,16 @@ class FactorizedSolver:
                 ec = grp.wrap["ec"]
                 ext = lay["U"] + en.ext
                 down_w.append(gemv(1, e, ec, _ext.mat(grp.wrap["pu_dev"], 0, ec), ext[None],
-                                   (lay["U"] + en.wrap.fine)[None]))
+                                   (lay["U"] + en.wrap.fine)[None], mk=(grp.depth, "wrapu"),
+                                   At=grp.wrap["pu_dev"][None]))
                 down_w.append(gemv(1, m3, ec, _ext.mat(grp.wrap["xsw"], 0, m3 + ec, off=m3), ext[None],
-                                   (lay["U"] + en.j3)[None], aidx=(lay["W"] + en.j3)[None]))
+                                   (lay["U"] + en.j3)[None], aidx=(lay["W"] + en.j3)[None],
+                                   mk=(grp.depth, "par"), At=grp.wrap["xsw"][None, :, m3:]))
                 continue
             ext = np.stack([lay["U"] + plan.node[n].ext_mergeorder for n in grp.ids])
             j3 = np.stack([plan.node[n].j3 for n in grp.ids])
             down_w.append(gemv(len(grp.ids), m3, e, _ext.mat(grp.xs, m3 * (m3 + e), m3 + e, off=m3), ext,
-                               lay["U"] + j3, aidx=lay["W"] + j3))
+                               lay["U"] + j3, aidx=lay["W"] + j3, mk=(grp.depth, "par"), At=grp.xs[:, :, m3:]))
         # leaves: u_c[i_ci] = [F | S] [g; u_ext], fused tail stage u_c[i_ce] = L u_ext  (solver.py:325-327)
         for gi, grp in enumerate(self.leaf_groups):
             L = len(grp.ids)
@@ -859,6 +962,11 @@ class FactorizedSolver:
         # split-K for steps with long rows and too few CTAs (top of the tree): partial products
         # into scratch pool rows, then a deterministic reduction step (A = ones)
         scratch = [lay["rows"]]
+        # two pool rows for padded level batching: ZERO (never written) and TRASH (padding outputs)
+        zero_row, trash_row = scratch[0], scratch[0] + 1
+        scratch[0] += 2
+        up, down, wonly, down_w = (self._merge_levels(lst, gemv, zero_row, trash_row, keep)
+                                   for lst in (up, down, wonly, down_w))
 
         def split(spec):
             if spec["mode2"] not in (0, 3) or "patch" in spec:
