@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define HPS_ABI_VERSION 6
+#define HPS_ABI_VERSION 7
 
 enum hps_status { HPS_OK = 0, HPS_EINVAL = 1, HPS_ECUDA = 2 };
 
@@ -155,6 +155,10 @@ typedef struct {
   int kparts;           /* 0/1: item i is A_i (R x K). kparts > 1 (split-K): item i is the column
                            block [(i % kparts) K, (i % kparts + 1) K) of operator A_{i / kparts},
                            which A describes unsplit (base/stride/ld/off, no ptrs) */
+  int kscale;           /* > 0: the gathered x_i[k] of columns k < kscale are multiplied by xscale
+                           (backward Euler: the body load g = u_n / dt is read straight from the
+                           leaf tabulations). Multi-RHS (nrhs >= 3) steps only. */
+  double xscale;
 } hps_gemv_batch;
 int hps_sweep_gemv(const hps_gemv_batch* g, void* stream);
 

@@ -44,7 +44,8 @@ class GemvBatch(C.Structure):
                 ("A", MatBatch), ("pool", C.c_void_p), ("xidx", C.c_void_p),
                 ("x2idx", C.c_void_p), ("aidx", C.c_void_p), ("oidx", C.c_void_p),
                 ("mode2", C.c_int), ("R2", C.c_int), ("K2", C.c_int), ("A2", MatBatch),
-                ("a2idx", C.c_void_p), ("o2idx", C.c_void_p), ("kparts", C.c_int)]
+                ("a2idx", C.c_void_p), ("o2idx", C.c_void_p), ("kparts", C.c_int),
+                ("kscale", C.c_int), ("xscale", C.c_double)]
 
 
 class LeafApplyArgs(C.Structure):
@@ -58,7 +59,7 @@ EXPORTS = ("hps_abi_version", "hps_status_string", "hps_gemm_batched", "hps_gj_w
            "hps_gj_invert_batched", "hps_leaf_workspace_bytes", "hps_leaf_build",
            "hps_merge_workspace_bytes", "hps_merge_build", "hps_sweep_gemv", "hps_leaf_apply")
 
-ABI_VERSION = 6
+ABI_VERSION = 7
 _lib = None
 _lock = threading.Lock()
 

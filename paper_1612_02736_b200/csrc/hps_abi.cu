@@ -220,12 +220,15 @@ static int to_gemv_args(const hps_gemv_batch* gb, GemvArgs* out) {
   a.ostride = a.R;
   a.kparts = gb->kparts > 1 ? gb->kparts : 1;
   if (a.kparts > 1 && (gb->A.ptrs || a.nitems % a.kparts)) return HPS_EINVAL;
+  a.kscale = gb->kscale > 0 ? gb->kscale : 0;
+  a.xscale = gb->xscale;
+  if (a.kscale && (a.nrhs < 3 || a.kscale > a.K || a.kparts > 1)) return HPS_EINVAL;
   // HPS_PRE_INDEX (read once per process, host side only): bit mask of the kernels that load
   // their static gather indices before the programmatic-launch wait; a kernel argument, so no
   // device-symbol copy (and no legacy-stream work) ever happens inside a launch path
   static const int pre_mask = [] {
     const char* e = getenv("HPS_PRE_INDEX");
-    return e ? atoi(e) : 15;
+    return e ? atoi(e) : 31;  // bit 16: L2 prefetch of the operator rows in the multi-RHS DMMA kernels
   }();
   a.pre_mask = pre_mask;
   if (a.mode2 && (!a.o2idx || a.R2 <= 0 || a.K2 <= 0 || (a.mode2 == 1 && a.K2 > a.K) ||

@@ -103,6 +103,8 @@ struct GemvArgs {
   int pre_mask;      // which kernels load static gather indices before the launch wait
                      // (bit mask, HPS_PRE_INDEX, set per launch by launch_gemv_gather)
   int kparts;        // split-K: item i = column block i % kparts of operator i / kparts (ABI)
+  int kscale;        // x columns k < kscale are scaled by xscale after the gather (ABI)
+  double xscale;
 };
 // Operator rows of item i (split-K aware)
 __device__ __forceinline__ const double* gemv_a(const GemvArgs& a, int i) {

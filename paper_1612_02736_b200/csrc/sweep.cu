@@ -53,7 +53,8 @@ static void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
 template <int NRP, int GU = 8, bool PLAIN = false>
 __device__ __forceinline__ void gather_x(double* dst, int ld, const int* __restrict__ xi,
                                          const int* __restrict__ x2, const double* pool, int nrhs, int kc,
-                                         int kp, int tid = -1, int nth = 0) {
+                                         int kp, int tid = -1, int nth = 0, int ksc = 0, double sc = 1.0) {
+  // (ksc, sc): columns k < ksc of this chunk are scaled by sc (GemvArgs::kscale / xscale)
   // (tid, nth): the gathering thread group (default: the whole CTA)
   if (tid < 0) {
     tid = threadIdx.x;
@@ -76,6 +77,7 @@ __device__ __forceinline__ void gather_x(double* dst, int ld, const int* __restr
       const int e = e0 + u * nth, k = e / NRP, j = e - k * NRP;
       v[u] = i1[u] >= 0 ? pool[(long long)i1[u] * nrhs + j] : 0.0;
       if (i2[u] >= 0) v[u] -= pool[(long long)i2[u] * nrhs + j];
+      if (k < ksc) v[u] *= sc;
     }
 #pragma unroll
     for (int u = 0; u < GU; ++u) {
@@ -195,6 +197,19 @@ __global__ void __launch_bounds__(SW_THREADS) gemv_gather_kernel(GemvArgs a, int
 // reduced through shared memory. A fragments are streamed straight from global memory (each
 // lane group reads one 32-byte sector per row, 8 loads in flight per lane), X is gathered into
 // shared memory chunk by chunk with a padded stride (conflict-free B fragments).
+// L2 bulk prefetch of rows [r0, r1) of an item's operator (static data: issued before the
+// programmatic-launch wait, so the DMMA loop after it reads L2 instead of HBM); one request per
+// row, spread over the calling threads (tid of nth)
+__device__ __forceinline__ void prefetch_rows(const double* Ai, long long ld, int r0, int r1, int K, int tid,
+                                              int nth) {
+  for (int r = r0 + tid; r < r1; r += nth) {
+    const double* rp = Ai + (long long)r * ld;
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(rp) & ~(uintptr_t)15;
+    const uintptr_t hi = (reinterpret_cast<uintptr_t>(rp + K) + 15) & ~(uintptr_t)15;
+    prefetch_l2_bulk(reinterpret_cast<const void*>(lo), (unsigned)(hi - lo));
+  }
+}
+
 template <int NRP, bool VEC>
 __global__ void __launch_bounds__(256, 4) gemv_dmma_kernel(GemvArgs a, int rpc, int kchunk, int batch_off,
                                                             int stage_idx) {
@@ -228,6 +243,7 @@ __global__ void __launch_bounds__(256, 4) gemv_dmma_kernel(GemvArgs a, int rpc, 
 #pragma unroll
     for (int n = 0; n < NT; ++n) acc[i][n][0] = acc[i][n][1] = 0.0;
   pdl_trigger();
+  if (a.pre_mask & 16) prefetch_rows(Ai, lda, blockIdx.x * rpc, min(R, (int)(blockIdx.x + 1) * rpc), K, tid, blockDim.x);
   // stage_idx: the (static) gather indices go to shared memory before the launch wait, so after
   // it the x gather is one dependent global load per element instead of two
   int* sidx = reinterpret_cast<int*>(red + (size_t)(WK - 1) * WR * 32 * (4 * NT));
@@ -244,9 +260,11 @@ __global__ void __launch_bounds__(256, 4) gemv_dmma_kernel(GemvArgs a, int rpc, 
     const int kcp = VEC ? (kc + 7) & ~7 : (kc + 3) & ~3;
     __syncthreads();
     if (stage_idx)
-      gather_x<NRP, 4, true>(xs, XLD, sidx + k0, x2 ? sidx + K + k0 : nullptr, pool, nrhs, kc, kcp);
+      gather_x<NRP, 4, true>(xs, XLD, sidx + k0, x2 ? sidx + K + k0 : nullptr, pool, nrhs, kc, kcp, -1, 0,
+                             a.kscale - k0, a.xscale);
     else
-      gather_x<NRP, 4>(xs, XLD, xi + k0, x2 ? x2 + k0 : nullptr, pool, nrhs, kc, kcp);
+      gather_x<NRP, 4>(xs, XLD, xi + k0, x2 ? x2 + k0 : nullptr, pool, nrhs, kc, kcp, -1, 0, a.kscale - k0,
+                       a.xscale);
     __syncthreads();
     if (VEC) {
       const int step = WK * 8;
@@ -393,18 +411,21 @@ __global__ void __launch_bounds__(256) gemv_dmma_multi_kernel(GemvArgs a) {
   const int* xi = a.xidx + (long long)(live ? item : 0) * a.xstride;
   const int* x2 = a.x2idx ? a.x2idx + (long long)(live ? item : 0) * a.xstride : nullptr;
   const int gtid = (int)threadIdx.x - grp * GW * 32;
-  if (live)
+  if (live) {
     for (int k = gtid; k < K; k += GW * 32) {
       sidx[k] = __ldg(xi + k);
       sidx[kp + k] = x2 ? __ldg(x2 + k) : -1;
     }
+    if (a.pre_mask & 16) prefetch_rows(gemv_a(a, item), a.A.ld, 0, R, K, gtid, GW * 32);
+  }
   pdl_wait();
   if (!live) return;  // whole group
   if (GW == 1)
     __syncwarp();
   else
     asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "r"(GW * 32) : "memory");
-  gather_x<NRP, 4, true>(xs, XLD, sidx, x2 ? sidx + kp : nullptr, a.pool, nrhs, K, kp, gtid, GW * 32);
+  gather_x<NRP, 4, true>(xs, XLD, sidx, x2 ? sidx + kp : nullptr, a.pool, nrhs, K, kp, gtid, GW * 32, a.kscale,
+                         a.xscale);
   if (GW == 1)
     __syncwarp();
   else

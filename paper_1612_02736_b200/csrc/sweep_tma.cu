@@ -228,8 +228,13 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1)
   unsigned ph = 0;
   int it = 0;
   for (int item = blockIdx.x; item < a.nitems; item += gridDim.x, ++it) {
-    const double* xc = xbuf + (size_t)(it & 1) * kp * XLD;
+    double* xc = xbuf + (size_t)(it & 1) * kp * XLD;
     double* xn = xbuf + (size_t)((it + 1) & 1) * kp * XLD;
+    if (a.kscale > 0) {
+      // backward Euler: the first kscale gathered columns (the body load u_n) times 1/dt
+      for (int e = tid; e < a.kscale * NRP; e += NC * 32) xc[(e / NRP) * XLD + (e % NRP)] *= a.xscale;
+      consumers_sync<NC>();
+    }
     // two accumulator sets (even / odd k4 steps): twice the independent DMMA chains per warp
     double acc[2][MT][NT][2];
 #pragma unroll
@@ -794,8 +799,13 @@ bool launch_gemv_stream(const GemvArgs& a, cudaStream_t s) {
     const char* e = getenv("HPS_STREAM_MIN_KB");
     return 1024LL * (e ? atoll(e) : 48);
   }();
-  if (!on || a.nrhs <= 2 || a.nrhs > 16 || a.A.ptrs || a.mode2 == 2) return false;
+  if (!on || a.nrhs <= 2 || a.nrhs > 16 || a.A.ptrs || a.mode2 == 2 || a.kscale) return false;
   if (a.R < 32 || a.K < 64 || 8LL * a.R * a.K < min_bytes) return false;
+  // where it measured faster than the register-streaming DMMA kernels (config 5, 16 RHS): the
+  // split-output downward steps of the upper-middle levels and the split-K parts of the top
+  // levels; HPS_STREAM=2 routes every eligible step here
+  if (on == 1 && !((a.mode2 == 3 && a.R >= 96 && 8LL * a.R * a.K >= 512 * 1024) || (a.kparts > 1 && a.R >= 1536)))
+    return false;
   if (a.mode2 == 3 && (a.K2 % 4 != 0 || a.kparts > 1)) return false;
   // mode2 = 1 (tail): a level-shared A2, at most one 8-row tile per consumer warp, K2 % 4 == 0,
   // and the tail's x columns inside the last 128-column x chunk

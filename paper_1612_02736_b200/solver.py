@@ -757,7 +757,7 @@ class FactorizedSolver:
 
     use_graphs = True
 
-    def _steps(self, prog, phase="full", leaves_down=True):
+    def _steps(self, prog, phase="full", leaves_down=True, parity=0):
         """Enqueue one solve on the current stream (leaves_down=False: everything but the final
         leaf step, see _run_overlapped). phase "full": upward sweep, f, downward sweep; "up": the
         upward pass alone (upward_pass); "down": the downward pass alone from the w and g rows
@@ -777,13 +777,14 @@ class FactorizedSolver:
             # needs no clearing: every u row is written (root exterior by the Dirichlet copy,
             # each J3 set by its parent) and w rows outside the J3 sets are never written
             pool[:2 * N].zero_()
-        for step in prog["up"]:
+        up_steps, all_down = (prog["up1"], prog["down1"]) if parity else (prog["up"], prog["down"])
+        for step in up_steps:
             _ext.check(lib.hps_sweep_gemv(step, s), "upward sweep")
         if phase == "up":
             for step in prog["wonly"]:
                 _ext.check(lib.hps_sweep_gemv(step, s), "upward sweep (w3)")
             return
-        down_steps = prog["down"] if leaves_down else prog["down"][:-len(self.leaf_groups)]
+        down_steps = all_down if leaves_down else all_down[:-len(self.leaf_groups)]
         # the Dirichlet copy onto u's root exterior runs on a forked stream (nothing in the
         # program reads it: readers take the f rows), joined before the program ends
         cur = torch.cuda.current_stream()
@@ -811,7 +812,7 @@ class FactorizedSolver:
             prog[key] = g
         return g
 
-    def _execute(self, prog, phase="full"):
+    def _execute(self, prog, phase="full", parity=0):
         if self.mode == "econ":
             lib = _ext.load()
             s = _stream_ptr()
@@ -822,16 +823,20 @@ class FactorizedSolver:
             # (operators are static while a program runs); the freshly rebuilt leaf operators
             # are published by one ordinary (non-PDL) launch between the build and the sweep
             prog.setdefault("fence", torch.zeros(1, dtype=torch.float64, device=self.device)).zero_()
-            self._steps(prog, phase)
+            self._steps(prog, phase, parity=parity)
             del fresh  # stream-ordered: the allocator reuses the blocks only for later work
             return
         if not (phase == "full" and self.use_graphs):
-            self._steps(prog, phase)
+            self._steps(prog, phase, parity=parity)
             return
-        self._graph(prog, "graph").replay()
+        self._graph(prog, "graph1" if parity else "graph", parity=parity).replay()
 
-    def _program(self, nrhs):
-        prog = self._sweeps.get(nrhs)
+    def _program(self, nrhs, be_alpha=None):
+        """Sweep program for nrhs right-hand sides. be_alpha (backward-Euler steppers, nrhs >= 3):
+        the leaf steps read the body load g = be_alpha * u_n straight from the leaf tabulations
+        (kscale / xscale of the C ABI), so no separate load-formation launch is needed."""
+        key = nrhs if be_alpha is None else (nrhs, "be", float(be_alpha))
+        prog = self._sweeps.get(key)
         if prog is not None:
             return prog
         self._prepare()
@@ -855,13 +860,36 @@ class FactorizedSolver:
         tree, plan = self.tree, self.plan
         # leaves: h = H g   (solver.py:278); H and F columns are in pivot order -> gather g by perm
         leaf_perm = [grp.perm.cpu().numpy().astype(np.int64) for grp in self.leaf_groups]
-        for gi, grp in enumerate(self.leaf_groups):
+        # scratch pool rows after the layout's regions (split-K partials, padding rows, ...)
+        scratch = [lay["rows"]]
+        # backward-Euler program: the leaf steps read g = alpha u_n from one tabulation region
+        # and write u_{n+1} to the other (two step lists, alternated by the stepper), so no
+        # launch ever reads rows it writes (a leaf's operator rows may span several CTAs)
+        uc_regions = (lay["UC"],)
+        if be_alpha is not None:
+            uc_regions = (lay["UC"], scratch[0])
+            scratch[0] += self._n_leaves * P
+
+        def gsrc(gi, grp, rows, src):
+            # pool rows of the body load in H / F column (pivot) order: the G region, or for a
+            # backward-Euler program the interior rows of the current leaf tabulations (scaled)
+            if be_alpha is None:
+                return lay["G"] + rows[:, None] * m + leaf_perm[gi]
+            return src + rows[:, None] * P + grp.sc.i_ci[leaf_perm[gi]]
+
+        def leaf_up(gi, grp, src):
             L = len(grp.ids)
             rows = grp.first_row + np.arange(L)
-            xidx = lay["G"] + rows[:, None] * m + leaf_perm[gi]
+            xidx = gsrc(gi, grp, rows, src)
             oidx = np.stack([hslot[n] + np.arange(b) for n in grp.ids])
-            up.append(gemv(L, b, m, _ext.mat(grp.h if grp.h is not None else 0, b * m, m), xidx, oidx))
-            up[-1]["patch"] = ("h", self.leaf_groups.index(grp))
+            st = gemv(L, b, m, _ext.mat(grp.h if grp.h is not None else 0, b * m, m), xidx, oidx)
+            st["patch"] = ("h", gi)
+            if be_alpha is not None:
+                st.update(kscale=m, xscale=float(be_alpha))
+            return st
+
+        for gi, grp in enumerate(self.leaf_groups):
+            up.append(leaf_up(gi, grp, uc_regions[0]))
         # parents, deepest first: h = Y d + [h_a[p1a]; h_b[p2b]], d = h_b[p3b] - h_a[p3a], Y = T_ei X
         # (solver.py:284-286 with the two GEMVs composed; X's columns are in pivot order, so d is
         # gathered through perm). w3 = X d is produced by the downward step (mode2 = 3); the
@@ -947,21 +975,32 @@ class FactorizedSolver:
             down_w.append(gemv(len(grp.ids), m3, e, _ext.mat(grp.xs, m3 * (m3 + e), m3 + e, off=m3), ext,
                                lay["U"] + j3, aidx=lay["W"] + j3, mk=(grp.depth, "par"), At=grp.xs[:, :, m3:]))
         # leaves: u_c[i_ci] = [F | S] [g; u_ext], fused tail stage u_c[i_ce] = L u_ext  (solver.py:325-327)
-        for gi, grp in enumerate(self.leaf_groups):
+        def leaf_down(gi, grp, src, dst):
             L = len(grp.ids)
             rows = grp.first_row + np.arange(L)
             ext = np.stack([lay["U"] + plan.node[n].ext for n in grp.ids])
-            gx = lay["G"] + rows[:, None] * m + leaf_perm[gi]
-            base = lay["UC"] + rows[:, None] * P
-            down.append(gemv(L, m, m + b, _ext.mat(grp.fs if grp.fs is not None else 0, m * (m + b), m + b),
-                             np.concatenate([gx, ext], axis=1),
-                             base + grp.sc.i_ci[None, :], mode2=1, R2=c, K2=b,
-                             A2=_ext.mat(grp.consts["lift"], 0, b), o2idx=base + grp.sc.i_ce[None, :]))
-            down[-1]["patch"] = ("fs", self.leaf_groups.index(grp))
+            gx = gsrc(gi, grp, rows, src)
+            base = dst + rows[:, None] * P
+            st = gemv(L, m, m + b, _ext.mat(grp.fs if grp.fs is not None else 0, m * (m + b), m + b),
+                      np.concatenate([gx, ext], axis=1),
+                      base + grp.sc.i_ci[None, :], mode2=1, R2=c, K2=b,
+                      A2=_ext.mat(grp.consts["lift"], 0, b), o2idx=base + grp.sc.i_ce[None, :])
+            st["patch"] = ("fs", gi)
+            if be_alpha is not None:
+                st.update(kscale=m, xscale=float(be_alpha))
+            return st
+
+        for gi, grp in enumerate(self.leaf_groups):
+            down.append(leaf_down(gi, grp, uc_regions[0], uc_regions[-1]))
             down_w.append(dict(down[-1]))
+        # backward Euler, odd steps: read the second region, write the first
+        up1 = down1 = None
+        if be_alpha is not None:
+            ng = len(self.leaf_groups)
+            up1 = [leaf_up(gi, grp, uc_regions[1]) for gi, grp in enumerate(self.leaf_groups)]
+            down1 = [leaf_down(gi, grp, uc_regions[1], uc_regions[0]) for gi, grp in enumerate(self.leaf_groups)]
         # split-K for steps with long rows and too few CTAs (top of the tree): partial products
         # into scratch pool rows, then a deterministic reduction step (A = ones)
-        scratch = [lay["rows"]]
         # two pool rows for padded level batching: ZERO (never written) and TRASH (padding outputs)
         zero_row, trash_row = scratch[0], scratch[0] + 1
         scratch[0] += 2
@@ -1064,7 +1103,7 @@ class FactorizedSolver:
         # the critical path (a forked branch of the program, joined at its end; _steps)
         lut = np.full(scratch[0] + 1, -1, dtype=np.int64)
         lut[lay["U"] + root_ext] = f_rows + np.arange(root_ext.size)
-        for sp in down:
+        for sp in down + (down1 or []):
             for k in ("xidx", "x2idx", "aidx"):
                 arr = sp.get(k)
                 if arr is None:
@@ -1082,13 +1121,30 @@ class FactorizedSolver:
             A2 = spec["A2"] if spec["A2"] is not None else _ext.MatBatch()
             return _ext.GemvBatch(spec["nitems"], spec["R"], spec["K"], nrhs, spec["A"], pool.data_ptr(),
                                   xi.data_ptr(), _ext.ptr(x2), _ext.ptr(ai), oi.data_ptr(), spec["mode2"],
-                                  spec["R2"], spec["K2"], A2, _ext.ptr(a2), _ext.ptr(o2), spec.get("kparts", 0))
+                                  spec["R2"], spec["K2"], A2, _ext.ptr(a2), _ext.ptr(o2), spec.get("kparts", 0),
+                                  spec.get("kscale", 0), spec.get("xscale", 1.0))
 
-        patches = [(k, i, s_["patch"]) for k, lst in (("up", up), ("down", down), ("down_w", down_w))
-                   for i, s_ in enumerate(lst) if "patch" in s_]
         ng = len(self.leaf_groups)
-        up = [build(s_) for s_ in up]
-        down = [build(s_) for s_ in down]
+        if up1 is not None:
+            # odd-step lists: the same parent steps around the swapped-region leaf steps
+            up1 = up1 + up[ng:]
+            down1 = down[:len(down) - ng] + down1
+        patches = [(k, i, s_["patch"]) for k, lst in (("up", up), ("down", down), ("down_w", down_w),
+                                                      ("up1", up1 or []), ("down1", down1 or []))
+                   for i, s_ in enumerate(lst) if "patch" in s_]
+        built = {}
+
+        def build_once(spec):
+            # the parent steps are shared by both step lists of a backward-Euler program
+            if id(spec) not in built:
+                built[id(spec)] = build(spec)
+            return built[id(spec)]
+
+        up = [build_once(s_) for s_ in up]
+        down = [build_once(s_) for s_ in down]
+        if up1 is not None:
+            up1 = [build_once(s_) for s_ in up1]
+            down1 = [build_once(s_) for s_ in down1]
         copy_f = build(copy_f)
         # leaf downward step as leaf-range launches (host-API path, _run_overlapped)
         leaf_chunks = []
@@ -1113,8 +1169,9 @@ class FactorizedSolver:
         prog = {"pool": pool, "up": up, "down": down, "wonly": wonly, "down_w": down_w, "keep": keep,
                 "f_in": f_in, "copy_f": copy_f,
                 "leaf_chunks": leaf_chunks,
-                "graph": None, "patches": patches}
-        self._sweeps[nrhs] = prog
+                "graph": None, "patches": patches,
+                "up1": up1, "down1": down1, "uc_regions": uc_regions}
+        self._sweeps[key] = prog
         return prog
 
 

@@ -14,6 +14,7 @@ that never leave HBM) followed by one replay of the CUDA-graph solve. Multi-RHS 
 from __future__ import annotations
 
 import csv
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -163,8 +164,15 @@ class DeviceStepper:
         self.ctx = ctx if ctx is not None else RhsContext(None, solver.tree, solver.p, solver.q, solver.device)
         if self.ctx.leaf_ids != list(solver._leaf_ids):
             raise ValueError("time-stepping context and solver disagree on the leaf order")
-        self.prog = solver._program(nrhs)
+        # backward Euler with several right-hand sides: the solve's leaf steps read g = alpha u_n
+        # straight from the leaf tabulations (one launch and 2 m doubles per leaf per RHS saved);
+        # Crank-Nicolson (beta != 0) forms its load with hps_leaf_apply
+        self.fold = beta == 0.0 and nrhs >= 3 and os.environ.get("HPS_BE_FOLD", "1") != "0"
+        self.prog = solver._program(nrhs, be_alpha=alpha if self.fold else None)
         self.lay = solver._layout
+        # folded program: the state alternates between two tabulation regions (parity = the
+        # region holding the current state, read by the next step)
+        self.parity = 0
 
     @property
     def pool(self):
@@ -174,7 +182,8 @@ class DeviceStepper:
         """(n_leaves, P, nrhs) view of the current leaf solutions (leaf-row order)."""
         s = self.solver
         P = s.p ** 2
-        return self.pool[self.lay["UC"]:self.lay["UC"] + s._n_leaves * P].view(s._n_leaves, P, self.nrhs)
+        r0 = self.prog["uc_regions"][self.parity]
+        return self.pool[r0:r0 + s._n_leaves * P].view(s._n_leaves, P, self.nrhs)
 
     def set_state(self, u_tabs: torch.Tensor):
         self.leaf_tabulations().copy_(u_tabs.reshape(self.leaf_tabulations().shape))
@@ -182,10 +191,15 @@ class DeviceStepper:
     def step(self, f: torch.Tensor):
         """Advance one step with Dirichlet data f ((|root ext|, nrhs), device) at t_{n+1}."""
         s, lay, n = self.solver, self.lay, self.nrhs
-        base = self.pool.data_ptr()
-        self.ctx.apply_ptr(base + 8 * n * lay["UC"], base + 8 * n * lay["G"], n, self.alpha, self.beta)
+        if not self.fold:
+            base = self.pool.data_ptr()
+            self.ctx.apply_ptr(base + 8 * n * lay["UC"], base + 8 * n * lay["G"], n, self.alpha, self.beta)
         self.prog["f_in"].copy_(f.reshape(-1, self.nrhs))
-        self.solver._execute(self.prog)
+        if self.fold:
+            self.solver._execute(self.prog, parity=self.parity)
+            self.parity ^= 1
+        else:
+            self.solver._execute(self.prog)
 
 
 def _leaf_points(solver: FactorizedSolver) -> np.ndarray:
