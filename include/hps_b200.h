@@ -152,9 +152,10 @@ typedef struct {
   hps_mat_batch A2;
   const int* a2idx;
   const int* o2idx;
-  int kparts;           /* 0/1: item i is A_i (R x K). kparts > 1 (split-K): item i is the column
-                           block [(i % kparts) K, (i % kparts + 1) K) of operator A_{i / kparts},
-                           which A describes unsplit (base/stride/ld/off, no ptrs) */
+  int kparts;           /* 0/1: item i is A_i (R x K). kparts > 1 (split-K, nrhs >= 3): item i is
+                           the column block [(i % kparts) K, (i % kparts + 1) K) of operator
+                           A_{i / kparts}, which A describes unsplit (base/stride/ld/off, no ptrs);
+                           single-RHS split-K parts are addressed through A.ptrs instead */
   int kscale;           /* > 0: the gathered x_i[k] of columns k < kscale are multiplied by xscale
                            (backward Euler: the body load g = u_n / dt is read straight from the
                            leaf tabulations). Multi-RHS (nrhs >= 3) steps only. */

@@ -219,7 +219,7 @@ static int to_gemv_args(const hps_gemv_batch* gb, GemvArgs* out) {
   a.xstride = a.K;
   a.ostride = a.R;
   a.kparts = gb->kparts > 1 ? gb->kparts : 1;
-  if (a.kparts > 1 && (gb->A.ptrs || a.nitems % a.kparts)) return HPS_EINVAL;
+  if (a.kparts > 1 && (gb->A.ptrs || a.nitems % a.kparts || a.nrhs <= 2)) return HPS_EINVAL;
   a.kscale = gb->kscale > 0 ? gb->kscale : 0;
   a.xscale = gb->xscale;
   if (a.kscale && (a.nrhs < 3 || a.kscale > a.K || a.kparts > 1)) return HPS_EINVAL;

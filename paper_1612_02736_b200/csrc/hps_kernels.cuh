@@ -49,6 +49,9 @@ int gj_fused_panel_width(int n, int full);
 bool gj_cluster_ok(int n, int nb);
 int launch_gj_cluster(int batch, int n, int k0, int nb, MatB M, int* piv, int* status, cudaStream_t s);
 int launch_gj_fused(const FusedArgs& a, int grid, cudaStream_t s);
+// small matrices resident in a 2-CTA cluster's shared memory (gj_pair.cu; full mode)
+bool gj_pair_ok(int n, int ncols);
+int launch_gj_pair(const FusedArgs& a, cudaStream_t s);
 
 // Leaf-stage assembly: interior rows of the collocation matrix for each leaf.
 struct LeafAsmArgs {
@@ -106,7 +109,8 @@ struct GemvArgs {
   int kscale;        // x columns k < kscale are scaled by xscale after the gather (ABI)
   double xscale;
 };
-// Operator rows of item i (split-K aware)
+// Operator rows of item i, split-K aware (multi-RHS kernels; the single-RHS kernels address
+// split-K parts through per-part pointer arrays, which keeps their hot loops branch-free)
 __device__ __forceinline__ const double* gemv_a(const GemvArgs& a, int i) {
   return a.kparts > 1 ? a.A.get(i / a.kparts) + (long long)(i % a.kparts) * a.K : a.A.get(i);
 }

@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(SW_THREADS) gemv_gather_kernel(GemvArgs a, int
   const int R = a.R, K = a.K, nrhs = a.nrhs;
   const int r0 = blockIdx.x * rows_per_cta;
   const int r1 = min(R, r0 + rows_per_cta);
-  const double* Ai = gemv_a(a, item);
+  const double* Ai = a.A.get(item);
   const long long lda = a.A.ld;
   const int* xi = a.xidx + (long long)item * a.xstride;
   const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
@@ -683,7 +683,7 @@ __device__ __forceinline__ void sweep_unit(const GemvArgs& a, int item, int chun
   const int* xi = a.xidx + (long long)item * a.xstride;
   const int* x2 = a.x2idx ? a.x2idx + (long long)item * a.xstride : nullptr;
   const double* pool = a.pool;
-  const double* Ai = gemv_a(a, item);
+  const double* Ai = a.A.get(item);
   const int r0 = chunk * rows_per_cta;
   const int r1 = min(a.R, r0 + rows_per_cta);
   __shared__ __align__(8) uint64_t sa_bar;
@@ -796,7 +796,7 @@ __global__ void __launch_bounds__(256) sweep_multi_kernel(GemvArgs a, int batch_
   __shared__ __align__(8) uint64_t sa_bars[IPC];
   pdl_trigger();
   const bool live = item < a.nitems;
-  const double* Ai = live ? gemv_a(a, item) : nullptr;
+  const double* Ai = live ? a.A.get(item) : nullptr;
   int shift = 0;
   if (SA && live) {
     const uintptr_t src = reinterpret_cast<uintptr_t>(Ai);
@@ -1091,7 +1091,7 @@ __global__ void __launch_bounds__(256) gemv_row1_kernel(GemvArgs a) {
     }
   }
   if (!live) return;
-  const double* A = gemv_a(a, item);
+  const double* A = a.A.get(item);
   double acc = 0.0;
 #pragma unroll
   for (int k = 0; k < KP; ++k) {

@@ -1054,9 +1054,20 @@ class FactorizedSolver:
             scr0 = scratch[0]
             scratch[0] += n * ns * R
             t = np.arange(n * ns)
-            # split-K parts: item i * ns + s = column block s of operator item i (ABI kparts)
+            # split-K parts: item i * ns + s = column block s of operator item i; multi-RHS steps
+            # describe them by ABI kparts, single-RHS steps by a per-part pointer array (their
+            # kernels keep a branch-free item addressing)
             part = dict(spec)
-            part.update(nitems=n * ns, K=kc, kparts=ns,
+            if nrhs > 2:
+                part.update(kparts=ns)
+            else:
+                A = spec["A"]
+                ptrs = np.array([A.base + 8 * (i * A.stride + A.off + s_ * kc) for i in range(n) for s_ in range(ns)],
+                                dtype=np.int64)
+                ptr_t = torch.as_tensor(ptrs, device=self.device)
+                keep.append(ptr_t)
+                part.update(A=_ext.MatBatch(0, 0, ptr_t.data_ptr(), A.ld, 0))
+            part.update(nitems=n * ns, K=kc,
                         xidx=spec["xidx"].reshape(n, ns, kc).reshape(n * ns, kc),
                         x2idx=None if spec["x2idx"] is None else spec["x2idx"].reshape(n * ns, kc),
                         aidx=None, oidx=scr0 + t[:, None] * R + np.arange(R)[None, :],
