@@ -28,6 +28,7 @@
 // the right-hand-side columns multiplied by the inverse, LAPACK pivots, |A^-1|_1, status flags.
 #include <cooperative_groups.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "hps_common.cuh"
@@ -174,9 +175,25 @@ __device__ __forceinline__ void gp_apply(double* Ms, int n, int k0, int kb, cons
 // rows lane + 32 s (s < GP_RPL) live in registers, the overflow rows GP_RPL*32 + lane (n up to
 // 32 (GP_RPL + 1)) are updated in place in shared memory; per column: argmax with the LAPACK tie
 // rule, interchange, scaling, elimination. Returns the status flag (zero / NaN pivot).
+#ifdef GP_TRACE
+// phase timestamps (clock64) of the first item of cluster 0, printed after the item: debug only
+__device__ long long gp_tr[2][2][32][8];
+#define GP_T(tag, p)                                                                   \
+  if (blockIdx.x < 2 && item == 0 && (threadIdx.x == 0 || threadIdx.x == 32) && (p) < 32) \
+    gp_tr[blockIdx.x][threadIdx.x >> 5][(p)][(tag)] = clock64();
+__device__ long long gp_tf[32][8][6];
+#define GP_F(tag) if (gp_trc) gp_tf[k0 >> 3][j][(tag)] = clock64();
+#else
+#define GP_F(tag)
+#define GP_T(tag, p)
+#endif
+
 __device__ __forceinline__ int gp_factor_warp(double* Ms, double* prow, int n, int k0, int kb, int pc0, int* spiv,
                                               int* piv_s) {
   const int lane = threadIdx.x & 31;
+#ifdef GP_TRACE
+  const bool gp_trc = blockIdx.x == 0 && lane == 0 && k0 < 256;
+#endif
   const int rx = GP_RPL * 32 + lane;  // overflow row of this lane (shared memory)
   double v[GP_RPL][GP_NB];
 #pragma unroll
@@ -191,6 +208,7 @@ __device__ __forceinline__ int gp_factor_warp(double* Ms, double* prow, int n, i
   for (int j = 0; j < GP_NB; ++j) {
     if (j >= kb) break;
     const int cj = k0 + j;
+    GP_F(0)
     double best = -1.0;
     int bi = n;
 #pragma unroll
@@ -218,6 +236,7 @@ __device__ __forceinline__ int gp_factor_warp(double* Ms, double* prow, int n, i
         bi = oi;
       }
     }
+    GP_F(1)
     const int pr = bi >= n ? cj : bi;  // all NaN: keep the diagonal, NaN propagates
     if (!(best > 0.0)) flag = 1;
     // rows pr (the pivot row) and cj (moves to pr) through shared memory, from their owner lanes
@@ -231,14 +250,18 @@ __device__ __forceinline__ int gp_factor_warp(double* Ms, double* prow, int n, i
 #pragma unroll
         for (int c = 0; c < GP_NB; ++c) crow[c] = v[s][c];
     }
+    // (overflow rows: only the kb panel columns are read or written; the rest of the 8-column
+    // window may belong to other columns of the matrix, updated concurrently by other warps)
     if (sp >= GP_RPL && lane == (pr & 31))
 #pragma unroll
-      for (int c = 0; c < GP_NB; ++c) prow[c] = Ms[sw(pr, pc0 + c)];
+      for (int c = 0; c < GP_NB; ++c) prow[c] = c < kb ? Ms[sw(pr, pc0 + c)] : 0.0;
     if (sc >= GP_RPL && lane == (cj & 31))
 #pragma unroll
-      for (int c = 0; c < GP_NB; ++c) crow[c] = Ms[sw(cj, pc0 + c)];
+      for (int c = 0; c < GP_NB; ++c) crow[c] = c < kb ? Ms[sw(cj, pc0 + c)] : 0.0;
     __syncwarp();
+    GP_F(2)
     const double inv = 1.0 / prow[j];
+    GP_F(3)
 #pragma unroll
     for (int s = 0; s < GP_RPL; ++s) {
       const int r = lane + 32 * s;
@@ -256,18 +279,20 @@ __device__ __forceinline__ int gp_factor_warp(double* Ms, double* prow, int n, i
 #pragma unroll
       for (int c = 0; c < GP_NB; ++c) v[s][c] = (c == j ? 0.0 : v[s][c]) - f * ((c == j) ? inv : prow[c] * inv);
     }
+    GP_F(4)
     if (rx < n) {
       if (rx == cj) {
 #pragma unroll
-        for (int c = 0; c < GP_NB; ++c) Ms[sw(rx, pc0 + c)] = (c == j) ? inv : prow[c] * inv;
+        for (int c = 0; c < GP_NB; ++c)
+          if (c < kb) Ms[sw(rx, pc0 + c)] = (c == j) ? inv : prow[c] * inv;
       } else {
         double w[GP_NB];
 #pragma unroll
-        for (int c = 0; c < GP_NB; ++c) w[c] = (rx == pr) ? crow[c] : Ms[sw(rx, pc0 + c)];
+        for (int c = 0; c < GP_NB; ++c) w[c] = c >= kb ? 0.0 : ((rx == pr) ? crow[c] : Ms[sw(rx, pc0 + c)]);
         const double f = w[j];
 #pragma unroll
         for (int c = 0; c < GP_NB; ++c)
-          Ms[sw(rx, pc0 + c)] = (c == j ? 0.0 : w[c]) - f * ((c == j) ? inv : prow[c] * inv);
+          if (c < kb) Ms[sw(rx, pc0 + c)] = (c == j ? 0.0 : w[c]) - f * ((c == j) ? inv : prow[c] * inv);
       }
     }
     if (lane == 0) {
@@ -275,6 +300,7 @@ __device__ __forceinline__ int gp_factor_warp(double* Ms, double* prow, int n, i
       piv_s[cj] = pr;
     }
     __syncwarp();  // prow / crow are rewritten by the next column
+    GP_F(5)
   }
 #pragma unroll
   for (int s = 0; s < GP_RPL; ++s) {
@@ -287,6 +313,7 @@ __device__ __forceinline__ int gp_factor_warp(double* Ms, double* prow, int n, i
   __syncwarp();
   return flag;
 }
+
 
 __global__ void __launch_bounds__(GP_THREADS, 1) gj_pair_kernel(FusedArgs a, int C0) {
   extern __shared__ double sm[];
@@ -362,10 +389,12 @@ __global__ void __launch_bounds__(GP_THREADS, 1) gj_pair_kernel(FusedArgs a, int
       const bool own = owner_of(p) == rank;
       const bool own_next = p + 1 < npan && owner_of(p + 1) == rank;
       const int lk0 = k0 - c0;  // local column of panel p (owner)
+      GP_T(0, p)
       if (!own) {
         bar_wait(pready + b, ready_cnt[b] & 1u);  // P_p and its pivots landed in Pb[b]
         ++ready_cnt[b];
       }
+      GP_T(1, p)
       const int* pv = spiv + b * GP_NB;
       const double* P = own ? nullptr : Pb + (size_t)b * n * GP_NB;
       const int skip_lo = own ? lk0 : -1, skip_hi = own ? lk0 + kb : -1;
@@ -383,6 +412,7 @@ __global__ void __launch_bounds__(GP_THREADS, 1) gj_pair_kernel(FusedArgs a, int
         }
       }
       __syncthreads();
+      GP_T(2, p)
       // 2. apply panel p; the owner of panel p+1 factors it on warp 0 meanwhile
       if (own_next) {
         const int nk0 = k0 + GP_NB, nlk = nk0 - c0, nkb = min(GP_NB, n - nk0);
@@ -391,8 +421,11 @@ __global__ void __launch_bounds__(GP_THREADS, 1) gj_pair_kernel(FusedArgs a, int
             gp_apply<true>(Ms, n, k0, kb, nullptr, lk0, nlk, nlk + nkb, skip_lo, skip_hi, 0, 1, 0);
           else
             gp_apply<false>(Ms, n, k0, kb, P, 0, nlk, nlk + nkb, skip_lo, skip_hi, 0, 1, 0);
+          GP_T(3, p)
           flag |= gp_factor_warp(Ms, prow, n, nk0, nkb, nlk, spiv + ((p + 1) & 1) * GP_NB, piv_s);
+          GP_T(4, p)
           push(p + 1, nlk);
+          GP_T(5, p)
         } else {
           // columns [0, nlk) and [nlk + nkb, cw) on warps 1..7 (named barrier 1)
           if (own) {
@@ -409,12 +442,27 @@ __global__ void __launch_bounds__(GP_THREADS, 1) gj_pair_kernel(FusedArgs a, int
         else
           gp_apply<false>(Ms, n, k0, kb, P, 0, 0, cw, skip_lo, skip_hi, 0, GP_WARPS, 1);
       }
+      GP_T(6, p)
       __syncthreads();
       // 3. buffers (Pb, spiv)[p & 1] are done with: release them to the peer if it is the one
       //    that will fill them next (panel p + 2)
       if (tid == 0 && p + 2 < npan && owner_of(p + 2) != rank) bar_arrive_remote(pfree + b, peer);
     }
 
+#ifdef GP_TRACE
+    if (blockIdx.x == 0 && item == 0 && threadIdx.x == 0)
+      for (int q = 0; q < 8; ++q)
+        for (int j = 0; j < 8; ++j)
+          printf("GPF p=%d j=%d %lld %lld %lld %lld %lld %lld\n", q, j, gp_tf[q][j][0], gp_tf[q][j][1], gp_tf[q][j][2],
+                 gp_tf[q][j][3], gp_tf[q][j][4], gp_tf[q][j][5]);
+    if (blockIdx.x < 2 && item == 0 && (threadIdx.x == 0 || threadIdx.x == 32))
+      for (int q = 0; q < npan && q < 32; ++q)
+        printf("GPT r%d t%d p=%d %lld %lld %lld %lld %lld %lld %lld\n", (int)blockIdx.x, (int)threadIdx.x, q,
+               gp_tr[blockIdx.x][threadIdx.x >> 5][q][0], gp_tr[blockIdx.x][threadIdx.x >> 5][q][1],
+               gp_tr[blockIdx.x][threadIdx.x >> 5][q][2], gp_tr[blockIdx.x][threadIdx.x >> 5][q][3],
+               gp_tr[blockIdx.x][threadIdx.x >> 5][q][4], gp_tr[blockIdx.x][threadIdx.x >> 5][q][5],
+               gp_tr[blockIdx.x][threadIdx.x >> 5][q][6]);
+#endif
     // ---------------- epilogue: pivots, column order, |A^-1|_1, write back
     cluster.sync();  // both halves factored; piv_s complete on both sides
     {
@@ -479,10 +527,10 @@ __global__ void __launch_bounds__(GP_THREADS, 1) gj_pair_kernel(FusedArgs a, int
 size_t gj_pair_smem(int n) { return sizeof(double) * GpLayout(n).total_doubles(); }
 
 bool gj_pair_ok(int n, int ncols) {
-  static int on = -1;  // HPS_GJ_PAIR=0: the one-CTA fused kernel instead
+  static int on = -1;  // opt-in (HPS_GJ_PAIR=1): slower than the one-CTA fused kernel so far
   if (on < 0) {
     const char* e = getenv("HPS_GJ_PAIR");
-    on = e ? atoi(e) : 1;
+    on = e ? atoi(e) : 0;
   }
   const int C0 = (((ncols + 1) / 2) + 7) & ~7;
   return on && n <= 32 * (GP_RPL + 1) && n >= 64 && ncols >= n && C0 <= GP_LD && ncols <= 2 * C0 &&

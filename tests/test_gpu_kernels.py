@@ -66,7 +66,7 @@ def _gj(lib, M, n, ncols):
 
 
 @pytest.mark.parametrize("n,nrhs,batch", [(1, 0, 2), (5, 3, 4), (15, 90, 3), (33, 7, 2), (60, 240, 5),
-                                          (196, 60, 3), (196, 60, 300), (130, 500, 150), (300, 10, 2),
+                                          (196, 60, 3), (196, 60, 300), (100, 40, 50), (196, 0, 20), (130, 500, 150), (300, 10, 2),
                                           (900, 124, 1), (1000, 3000, 1), (1003, 37, 2), (1920, 200, 1)])
 def test_gj_inverse_matches_numpy(lib, n, nrhs, batch):
     rng = np.random.default_rng(n)
@@ -126,3 +126,16 @@ def test_gj_permuted_columns_output(lib, n, batch):
     for i in range(batch):
         inv = np.linalg.inv(A[i])
         assert np.abs(out[i] - inv[:, pm[i]]).max() <= 1e-11 * np.abs(inv).max()
+
+
+def test_gj_pair_kernel_opt_in():
+    """The 2-CTA cluster Gauss-Jordan kernel (csrc/gj_pair.cu, opt-in with HPS_GJ_PAIR=1, read once
+    per process) passes the same inverse / pivot / permuted-output checks."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, HPS_GJ_PAIR="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", __file__,
+                        "-k", "gj_inverse or gj_pivot or gj_permuted or gj_flags"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
