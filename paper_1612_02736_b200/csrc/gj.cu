@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(GJ_THREADS) gj_panel_kernel(int n, int k0, int
 // each column needs only independent loads: W[j] = M[rowid[k0+j]] and, for the displaced
 // rows outside the panel (which always receive original panel rows), M[x] = M[rowid[x]].
 // Rows inside the panel are not written: the GJ update overwrites them with panel_J W.
-__global__ void gj_swapcopy_kernel(int n, int col_lo, int col_hi, int k0, int kb, MatB M, const int* piv,
+__global__ void gj_swapcopy_kernel(int n, int col_lo, int nlog, int kskip, int k0, int kb, MatB M, const int* piv,
                                    MatB W, int batch_off) {
   extern __shared__ int rowid[];  // n - k0 entries + moves
   int* moves = rowid + (n - k0);  // [0] count, then (dst, src)
@@ -196,9 +196,9 @@ __global__ void gj_swapcopy_kernel(int n, int col_lo, int col_hi, int k0, int kb
   }
   __syncthreads();
   const int cl = blockIdx.x * blockDim.x + threadIdx.x;
-  if (cl >= (col_hi - col_lo) - kb) return;
+  if (cl >= nlog) return;
   int c = col_lo + cl;
-  if (c >= k0) c += kb;
+  if (c >= kskip) c += kb;  // the panel's own columns are skipped when they lie inside the range
   double* Mi = M.get(item);
   const long long ld = M.ld;
   double* Wi = W.get(item);
@@ -324,19 +324,20 @@ static int sm_count() {
 }
 
 
-// Row interchanges of the panel [k0, k0+kb) applied to the columns [col_lo, col_hi) \ panel,
-// saving the pivot rows to W.
+// Row interchanges of the panel [k0, k0+kb) applied to the columns [col_lo, col_hi) \ panel
+// (the panel may lie inside or outside the range), saving the pivot rows to W.
 static void swapcopy_range(int batch, int n, int col_lo, int col_hi, int k0, int kb, MatB M, const int* piv,
                            MatB W, cudaStream_t s) {
-  const int nlog = (col_hi - col_lo) - kb;
+  const bool inside = k0 >= col_lo && k0 < col_hi;
+  const int nlog = (col_hi - col_lo) - (inside ? kb : 0);
   if (nlog <= 0) return;
   for (int off = 0; off < batch; off += 65535) {
     const int bb = min(65535, batch - off);
     // one thread per column; few matrices: 32-thread CTAs so the pass spreads over the SMs
     const int nt = (long long)((nlog + 127) / 128) * bb >= 2 * sm_count() ? 128 : 32;
     dim3 g2((nlog + nt - 1) / nt, bb);
-    gj_swapcopy_kernel<<<g2, nt, sizeof(int) * (n - k0 + 2 * kb + 4), s>>>(n, col_lo, col_hi, k0, kb, M, piv,
-                                                                           W, off);
+    gj_swapcopy_kernel<<<g2, nt, sizeof(int) * (n - k0 + 2 * kb + 4), s>>>(n, col_lo, nlog, inside ? k0 : (1 << 30),
+                                                                           k0, kb, M, piv, W, off);
   }
 }
 
@@ -490,7 +491,15 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
     const int nb = min(NB, n - K0);
     const int K1 = K0 + nb;
     const int nb1 = min(NB, n - K1);
-    swapcopy_range(batch, n, 0, ncols, K0, nb, M, piv, W, s);
+    // with look-ahead the next block's columns get their interchanges + update first, so the
+    // side stream starts factoring them while the main stream swaps and updates all the others
+    // (the full-width interchange pass was ~35 us per block on the critical path of the top merges)
+    const bool early = use_la && nb1 > 0;
+    if (early) {
+      swapcopy_range(batch, n, K1, K1 + nb1, K0, nb, M, piv, W, s);
+    } else {
+      swapcopy_range(batch, n, 0, ncols, K0, nb, M, piv, W, s);
+    }
     if (nb1 > 0) {
       if ((rc = gemm_range(batch, n, K1, K1 + nb1, K0, nb, M, W, s))) return rc;
       if (use_la) {
@@ -498,6 +507,8 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
         cudaStreamWaitEvent(la.side, la.ev_a, 0);
         if ((rc = factor_block(batch, n, ncols, K1, nb1, scheme, M, piv, status, W, la.side))) return rc;
         cudaEventRecord(la.ev_b, la.side);
+        swapcopy_range(batch, n, 0, K1, K0, nb, M, piv, W, s);
+        swapcopy_range(batch, n, K1 + nb1, ncols, K0, nb, M, piv, W, s);
       }
     }
     if ((rc = gemm_range(batch, n, 0, K0, K0, nb, M, W, s))) return rc;
