@@ -67,15 +67,16 @@ int hps_gj_invert_batched(int batch, int n, int ncols, const hps_mat_batch* M, i
                    (cudaStream_t)stream, perm);
 }
 
-static long long colpart_bytes(int nleaf, int p) {
+static long long colpart_bytes(int nleaf, int p, int q) {
   const long long m = (long long)(p - 2) * (p - 2);
   if ((long long)p * p > 8 * 256) return 0;  // no fused |A_ii|_1 (leaf_merge.cu)
-  return align256(8LL * nleaf * ((m + leaf_assemble_rows() - 1) / leaf_assemble_rows()) * m);
+  const int rows = leaf_assemble_rows(p, q);
+  return align256(8LL * nleaf * ((m + rows - 1) / rows) * m);
 }
 
 long long hps_leaf_workspace_bytes(int nleaf, int p, int q) {
   const long long m = (long long)(p - 2) * (p - 2), b = 4LL * q, c = 4LL * (p - 1);
-  return align256(8 * nleaf * m * c) + align256(4 * nleaf * m) + colpart_bytes(nleaf, p) +
+  return align256(8 * nleaf * m * c) + align256(4 * nleaf * m) + colpart_bytes(nleaf, p, (int)q) +
          hps_gj_workspace_bytes(nleaf, (int)m, (int)(m + b));
 }
 
@@ -87,7 +88,7 @@ int hps_leaf_build(const hps_leaf_batch* L, void* stream) {
   char* ws = (char*)L->workspace;
   double* aie = (double*)ws;
   int* piv = (int*)(ws + align256(8ull * nl * m * c));
-  const long long cpb = colpart_bytes(nl, p);
+  const long long cpb = colpart_bytes(nl, p, q);
   double* colpart = cpb ? (double*)(ws + align256(8ull * nl * m * c) + align256(4ull * nl * m)) : nullptr;
   void* gjw = ws + align256(8ull * nl * m * c) + align256(4ull * nl * m) + cpb;
   const long long sfs = (long long)m * (m + b);
@@ -107,20 +108,23 @@ int hps_leaf_build(const hps_leaf_batch* L, void* stream) {
   // |A_ii|_1 (the rcond rule, leaf.py:113-115) from the assembly itself: no separate pass over A_ii
   a.colpart = L->anorm ? colpart : nullptr;
   a.anorm = L->anorm;
-  int rc = launch_leaf_assemble(a, s);
-  if (rc) return rc;
-
-  // right-hand sides of the interior solve: fs[:, m:] = -A_ie L   (leaf.py:154)
+  // assembly and the right-hand sides fs[:, m:] = -A_ie L (leaf.py:154) in one launch when the
+  // fused kernel applies (A_ie stays in shared memory), else assembly + a batched GEMM
   GemmArgs g{};
-  g.M = m;
-  g.N = b;
-  g.K = c;
-  g.alpha = -1.0;
-  g.beta = 0.0;
-  g.A = dense(aie, (long long)m * c, c);
-  g.B = dense(const_cast<double*>(L->lift), 0, b);
-  g.C = dense(L->fs, sfs, m + b, m);
-  if ((rc = launch_gemm(g, nl, MODE_GEMM, s))) return rc;
+  int rc = launch_leaf_assemble_fused(a, a.Aii, L->lift, q, s);
+  if (rc > 0) return rc;
+  if (rc < 0) {
+    if ((rc = launch_leaf_assemble(a, s))) return rc;
+    g.M = m;
+    g.N = b;
+    g.K = c;
+    g.alpha = -1.0;
+    g.beta = 0.0;
+    g.A = dense(aie, (long long)m * c, c);
+    g.B = dense(const_cast<double*>(L->lift), 0, b);
+    g.C = dense(L->fs, sfs, m + b, m);
+    if ((rc = launch_gemm(g, nl, MODE_GEMM, s))) return rc;
+  }
 
   // [F | S] = inv(A_ii) [I | -A_ie L]
   if ((rc = gj_invert(nl, m, m + b, dense(L->fs, sfs, m + b), piv, (double*)gjw, colpart ? nullptr : L->anorm,

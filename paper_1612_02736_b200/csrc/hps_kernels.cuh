@@ -68,8 +68,10 @@ struct LeafAsmArgs {
   double* colpart;         // nullable: [nleaf][row blocks][m] partial column sums of |A_ii|
   double* anorm;           // with colpart: |A_ii|_1 per leaf (leaf_assemble_rows() rows per block)
 };
-int leaf_assemble_rows();
+int leaf_assemble_rows(int p, int q);  // rows per CTA = row blocks of colpart
 int launch_leaf_assemble(const LeafAsmArgs& a, cudaStream_t s);
+// fused assembly + right-hand sides FS[:, m:] = -A_ie L (A_ie stays on chip); -1: not applicable
+int launch_leaf_assemble_fused(const LeafAsmArgs& a, MatB FS, const double* lift, int q, cudaStream_t s);
 
 // Merge gather: builds [Delta | -Ta31 | Tb32], Tei = [Ta13; Tb23], Tnew = blkdiag(Ta11, Tb22)
 struct MergeGatherArgs {

@@ -1,5 +1,8 @@
 // Leaf-stage assembly and merge-stage gather kernels (bandwidth-bound producers feeding the
 // DMMA Gauss-Jordan and GEMM kernels).
+#include <algorithm>
+#include <cstdlib>
+
 #include "hps_common.cuh"
 #include "hps_kernels.cuh"
 
@@ -106,7 +109,6 @@ __global__ void __launch_bounds__(256) leaf_assemble_kernel(LeafAsmArgs a, int b
   }
 }
 
-int leaf_assemble_rows() { return ASM_ROWS; }
 
 // |A_ii|_1 per leaf from the assembly's partial column sums (row blocks summed in order)
 __global__ void __launch_bounds__(256) colpart_norm_kernel(int m, int nrb, const double* colpart, double* anorm,
@@ -132,6 +134,311 @@ __global__ void __launch_bounds__(256) colpart_norm_kernel(int m, int nrb, const
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = (red[w] > v || red[w] != red[w]) ? red[w] : v;
     anorm[leaf] = v;
   }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Fused leaf assembly: one CTA builds `rows` complete rows [A_ii | A_ie] of one leaf in shared
+// memory (columns in output order: the m interior nodes, then the c exterior nodes), multiplies
+// the exterior part by the lift on DMMA tiles, R = -A_ie L (rows x b, leaf.py:154), and writes
+// [A_ii | R] as whole contiguous rows of the Gauss-Jordan workspace: A_ie never goes to HBM and
+// there is no separate GEMM launch (config 5: assembly 4.3 ms + GEMM 3.8 ms before).
+//
+// Only the 2p - 1 entries of a row that share a grid line with the row's node carry the
+// c11/c22/c1/c2/c terms; every other entry is the mixed-derivative term alone,
+//   -(2 c12) (dy[i2,j2] dx[i1,j1])
+// (the reference's accumulation order adds exact zeros there), so the bulk pass is two
+// multiplications per entry and a second pass recomputes the cross entries with the full,
+// reference-ordered expression.
+struct AsmFusedCfg {
+  int rows;     // rows per CTA (multiple of 8)
+  int ldt;      // tile row length in doubles (== 4 mod 16: conflict-free DMMA A fragments)
+  int b, c;     // Gauss edge nodes / exterior Chebyshev nodes
+  int vec;      // 16-byte row stores allowed
+  int csc;      // doubles reserved for the column-sum exchange (two row groups in the write-out)
+  const double* lift;
+  MatB FS;      // m x (m + b) per leaf
+};
+
+constexpr int ASMF_MAXT = 4;  // R tiles (8 x 8) held per warp
+
+__global__ void __launch_bounds__(256) leaf_assemble_fused_kernel(LeafAsmArgs a, AsmFusedCfg f, int nrb) {
+  extern __shared__ double sd[];
+  const int p = a.p, P = p * p, pm = p - 2;
+  const int m = pm * pm, b = f.b, c = f.c, rows = f.rows, ldt = f.ldt;
+  const int ncol = m + b;
+  double* dx = sd;
+  double* dy = dx + P;
+  double* dxx = dy + P;
+  double* dyy = dxx + P;
+  double* cr = dyy + P;                 // [rows][6] coefficient samples at the row points
+  double* csc = cr + 6 * rows;          // [ncol] column-sum exchange between the two row groups
+  double* T = csc + f.csc;              // [rows][ldt] output rows
+  int* jof = reinterpret_cast<int*>(T + (size_t)rows * ldt);  // output column -> grid node
+  int* qof = jof + P;                                          // grid node -> output column
+  int2* ri = reinterpret_cast<int2*>(qof + P);                 // [rows] row offsets (i1 p, i2 p) into the 1D operators
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long cstride = (long long)a.nleaf * P;
+  // static data once per CTA (persistent over (leaf, row block) units)
+  for (int e = tid; e < P; e += 256) {
+    dx[e] = a.dx[e];
+    dy[e] = a.dy[e];
+    dxx[e] = a.dxx[e];
+    dyy[e] = a.dyy[e];
+    const int ip = a.int_pos[e];
+    const int q = ip >= 0 ? ip : m + a.ext_pos[e];
+    qof[e] = q;
+    jof[q] = e;
+  }
+  const long long units = (long long)a.nleaf * nrb;
+  // coefficient samples of a unit: at most one value per thread (rows * 6 <= 256), fetched one
+  // unit ahead into a register
+  auto fetch = [&](long long u) -> double {
+    if (u >= units || tid >= rows * 6) return 0.0;
+    const int leaf = (int)(u / nrb), rb = (int)(u - (long long)leaf * nrb);
+    const int rr = tid / 6, t = tid - rr * 6, r = rb * rows + rr;
+    return r < m ? a.coef[(long long)leaf * P + t * cstride + (1 + r % pm) + p * (1 + r / pm)] : 0.0;
+  };
+  double cnext = fetch(blockIdx.x);
+  const int g = lane >> 2, t4 = lane & 3;
+  const int mtiles = rows >> 3, ntiles = (b + 7) >> 3, ntile = mtiles * ntiles;
+  const int np2 = ncol >> 1;
+  const int nh = f.csc ? 2 : 1;  // row groups of the write-out pass
+  for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+    const int leaf = (int)(u / nrb), rb = (int)(u - (long long)leaf * nrb);
+    const int r0 = rb * rows;
+    const int nr = min(rows, m - r0);
+    __syncthreads();  // previous unit's tile and coefficients fully consumed
+    if (tid < rows * 6) cr[tid] = cnext;
+    if (tid < rows) {
+      const int r = min(r0 + tid, m - 1);
+      ri[tid] = make_int2((1 + r % pm) * p, (1 + r / pm) * p);
+    }
+    cnext = fetch(u + gridDim.x);
+    __syncthreads();
+    // 1. bulk pass: thread owns output columns q = tid + 256 k
+    for (int q = tid; q < P; q += 256) {
+      const int j = jof[q], j2 = j / p, j1 = j - j2 * p;
+      // four rows per step, all loads before the stores (independent chains: the loop is
+      // latency-bound otherwise, shared-memory stores and loads may alias for the compiler)
+      int rr = 0;
+      for (; rr + 4 <= nr; rr += 4) {
+        double cc[4], vy[4], vx[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int2 io = ri[rr + k];
+          cc[k] = cr[(rr + k) * 6 + 1];
+          vy[k] = dy[io.y + j2];
+          vx[k] = dx[io.x + j1];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) T[(rr + k) * ldt + q] = -((2.0 * cc[k]) * (vy[k] * vx[k]));
+      }
+      for (; rr < nr; ++rr) {
+        const int2 io = ri[rr];
+        T[rr * ldt + q] = -((2.0 * cr[rr * 6 + 1]) * (dy[io.y + j2] * dx[io.x + j1]));
+      }
+    }
+    __syncthreads();
+    // 2. cross entries (same grid line as the row's node): the full expression, reference order
+    for (int e = tid; e < nr * (2 * p - 1); e += 256) {
+      const int rr = e / (2 * p - 1), sidx = e - rr * (2 * p - 1);
+      const int2 io = ri[rr];
+      const int i1 = io.x / p, i2 = io.y / p;
+      int j1, j2;
+      if (sidx < p) {
+        j1 = sidx;
+        j2 = i2;
+      } else {
+        j1 = i1;
+        j2 = sidx - p;
+        if (j2 >= i2) ++j2;
+      }
+      const double* c6 = cr + rr * 6;
+      const double d11 = (i2 == j2) ? dxx[io.x + j1] : 0.0;
+      const double d12 = dy[io.y + j2] * dx[io.x + j1];
+      const double d22 = (i1 == j1) ? dyy[io.y + j2] : 0.0;
+      const double d1 = (i2 == j2) ? dx[io.x + j1] : 0.0;
+      const double d2 = (i1 == j1) ? dy[io.y + j2] : 0.0;
+      double v = -(c6[0] * d11);
+      v -= 2.0 * c6[1] * d12;
+      v -= c6[2] * d22;
+      v += c6[3] * d1;
+      v += c6[4] * d2;
+      if (j1 == i1 && j2 == i2) v += c6[5];
+      T[rr * ldt + qof[j1 + p * j2]] = v;
+    }
+    __syncthreads();
+    // 3. R = -A_ie L on DMMA tiles (A_ie = T[:, m : m + c]); results held until every warp has
+    //    read its A_ie fragments, then written over the A_ie columns
+    double acc[ASMF_MAXT][2];
+    const double* arow[ASMF_MAXT];
+    const double* bcol[ASMF_MAXT];
+    bool bok[ASMF_MAXT];
+#pragma unroll
+    for (int k = 0; k < ASMF_MAXT; ++k) {
+      acc[k][0] = acc[k][1] = 0.0;
+      const int tile = min(warp + 8 * k, ntile - 1);  // surplus slots repeat the last tile (never stored)
+      const int mt = tile % mtiles, nt = tile / mtiles;
+      const int col = nt * 8 + g;
+      arow[k] = T + (size_t)(mt * 8 + g) * ldt + m + t4;
+      bok[k] = col < b;
+      bcol[k] = f.lift + (bok[k] ? col : 0) + (long long)t4 * b;
+    }
+    // k outer, tiles inner: up to ASMF_MAXT independent DMMA chains per warp
+    for (int kk = 0; kk < c; kk += 4) {
+      double av[ASMF_MAXT], bv[ASMF_MAXT];
+#pragma unroll
+      for (int k = 0; k < ASMF_MAXT; ++k) {
+        av[k] = arow[k][kk];
+        bv[k] = bok[k] ? __ldg(bcol[k] + (long long)kk * b) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < ASMF_MAXT; ++k) dmma8x8x4(acc[k][0], acc[k][1], av[k], bv[k]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < ASMF_MAXT; ++k) {
+      const int tile = warp + 8 * k;
+      if (tile < ntile) {
+        const int mt = tile % mtiles, nt = tile / mtiles;
+        double* drow = T + (size_t)(mt * 8 + g) * ldt + m + nt * 8 + 2 * t4;
+        if (nt * 8 + 2 * t4 < b) drow[0] = -acc[k][0];
+        if (nt * 8 + 2 * t4 + 1 < b) drow[1] = -acc[k][1];
+      }
+    }
+    __syncthreads();
+    // 4. whole rows [A_ii | R] -> global (coalesced); |A_ii|_1 partial column sums on the way
+    double* fs = f.FS.get(leaf);
+    const long long ld = f.FS.ld;
+    double* cp = a.colpart ? a.colpart + ((long long)leaf * nrb + rb) * m : nullptr;
+    if (f.vec && nh == 2) {
+      // thread = (row group h, column pair q2): all 256 threads store; the second group's
+      // column sums reach the first through csc
+      const int h = tid / np2, q = 2 * (tid - h * np2);
+      double s0 = 0.0, s1 = 0.0;
+      if (h < 2) {
+        for (int rr = h; rr < nr; rr += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(T + (size_t)rr * ldt + q);
+          *reinterpret_cast<double2*>(fs + (long long)(r0 + rr) * ld + q) = v;
+          s0 += fabs(v.x);
+          s1 += fabs(v.y);
+        }
+        if (h == 1) {
+          csc[q] = s0;
+          csc[q + 1] = s1;
+        }
+      }
+      __syncthreads();
+      if (h == 0 && cp) {
+        if (q < m) cp[q] = s0 + csc[q];
+        if (q + 1 < m) cp[q + 1] = s1 + csc[q + 1];
+      }
+    } else if (f.vec) {
+      for (int q2 = tid; q2 < np2; q2 += 256) {
+        const int q = 2 * q2;
+        double s0 = 0.0, s1 = 0.0;
+        for (int rr = 0; rr < nr; ++rr) {
+          const double2 v = *reinterpret_cast<const double2*>(T + (size_t)rr * ldt + q);
+          *reinterpret_cast<double2*>(fs + (long long)(r0 + rr) * ld + q) = v;
+          s0 += fabs(v.x);
+          s1 += fabs(v.y);
+        }
+        if (cp) {
+          if (q < m) cp[q] = s0;
+          if (q + 1 < m) cp[q + 1] = s1;
+        }
+      }
+    } else {
+      for (int q = tid; q < ncol; q += 256) {
+        double s0 = 0.0;
+        for (int rr = 0; rr < nr; ++rr) {
+          const double v = T[(size_t)rr * ldt + q];
+          fs[(long long)(r0 + rr) * ld + q] = v;
+          s0 += fabs(v);
+        }
+        if (cp && q < m) cp[q] = s0;
+      }
+    }
+  }
+}
+
+static int asm_fused_csc(int ncol) { return ncol <= 256 ? ((ncol + 1) & ~1) : 0; }
+static size_t asm_fused_smem(int P, int rows, int ncol) {
+  const int ldt = ((P + 15) & ~15) + 4;
+  return sizeof(double) * (4 * P + 6 * rows + asm_fused_csc(ncol) + (size_t)rows * ldt) +
+         sizeof(int) * (2 * P + 2 * rows);
+}
+
+// rows per CTA of the fused kernel for this leaf order (0: not applicable, use the two-kernel path)
+static int asm_fused_rows(int p, int b) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("HPS_ASM_FUSED");
+    on = e ? atoi(e) : 1;
+  }
+  if (!on) return 0;
+  const int P = p * p, m = (p - 2) * (p - 2), ntiles = (b + 7) / 8;
+  // measured on the B200: p = 16 leaves 5.7 -> 3.8 ms per 16384 (assembly + GEMM before), but
+  // p = 32 leaves 4.7 -> 6.1 ms per 1024 (8-row tiles, 2 CTAs per SM): large orders keep the
+  // two-kernel path (HPS_ASM_FUSED=2 forces the fused kernel for every order it fits)
+  if (on == 1 && P > 576) return 0;
+  static int rmax = -1;
+  if (rmax < 0) {
+    const char* e = getenv("HPS_ASM_ROWS");
+    rmax = e ? atoi(e) : 32;
+  }
+  for (int rows = rmax; rows >= 8; rows -= 8) {
+    if (rows / 8 * ntiles > 8 * ASMF_MAXT) continue;
+    if (asm_fused_smem(P, rows, m + b) <= (size_t)(rows == 8 ? 200 : 100) * 1024) return rows;  // >= 2 CTAs per SM unless only 8 rows fit
+  }
+  return 0;
+}
+
+int leaf_assemble_rows(int p, int q) {
+  const int r = asm_fused_rows(p, 4 * q);
+  return r ? r : ASM_ROWS;
+}
+
+// Assembly + right-hand sides in one launch; returns -1 when the fused kernel does not apply.
+int launch_leaf_assemble_fused(const LeafAsmArgs& a, MatB FS, const double* lift, int q, cudaStream_t s) {
+  const int p = a.p, P = p * p, m = (p - 2) * (p - 2), b = 4 * q, c = 4 * (p - 1);
+  const int rows = asm_fused_rows(p, b);
+  if (!rows || b > c || (a.colpart && P > 8 * 256)) return -1;
+  AsmFusedCfg f{};
+  f.rows = rows;
+  f.ldt = ((P + 15) & ~15) + 4;
+  f.b = b;
+  f.c = c;
+  f.lift = lift;
+  f.FS = FS;
+  f.vec = !FS.ptrs && FS.base && ((reinterpret_cast<uintptr_t>(FS.base) >> 3) & 1) == 0 &&
+          ((FS.stride | FS.off | (long long)FS.ld | (long long)(m + b)) & 1) == 0;
+  f.csc = f.vec ? asm_fused_csc(m + b) : 0;
+  const size_t smem = asm_fused_smem(P, rows, m + b);
+  static int sms = 0, max_smem = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(leaf_assemble_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    max_smem = 200 * 1024;
+  }
+  if (smem > (size_t)max_smem) return -1;
+  const int nrb = (m + rows - 1) / rows;
+  // persistent CTAs (the 1D operators and index maps are staged once per CTA): as many as fit
+  static int cap = -1;
+  if (cap < 0) {
+    const char* e = getenv("HPS_ASM_PER_SM");
+    cap = e ? atoi(e) : 4;
+  }
+  const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(cap, (227 * 1024) / (smem + 1024)));
+  const long long units = (long long)a.nleaf * nrb;
+  const int grid = (int)std::min<long long>(units, (long long)per_sm * sms);
+  leaf_assemble_fused_kernel<<<grid, 256, smem, s>>>(a, f, nrb);
+  if (a.colpart && a.anorm)
+    for (int off = 0; off < a.nleaf; off += 65535)
+      colpart_norm_kernel<<<min(65535, a.nleaf - off), 256, 0, s>>>(m, nrb, a.colpart, a.anorm, off);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
 int launch_leaf_assemble(const LeafAsmArgs& a, cudaStream_t s) {
