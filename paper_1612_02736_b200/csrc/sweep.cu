@@ -929,7 +929,12 @@ static int sweep_rows_per_cta(const GemvArgs& a) {
   if (a.mode2 != 2) {
     const int G = 32 / lanes_for(a.K);
     const int minrows = 8 * G * 2;
-    rows = a.R < 64 ? a.R : 64;
+    static int rcap = -1;  // HPS_ROWS_CAP: most rows per CTA (each CTA gathers its item's x once)
+    if (rcap < 0) {
+      const char* e = getenv("HPS_ROWS_CAP");
+      rcap = e ? atoi(e) : 64;
+    }
+    rows = a.R < rcap ? a.R : rcap;
     while (rows > minrows && (long long)a.nitems * ((a.R + rows - 1) / rows) < 4 * 148) rows = (rows + 1) / 2;
     if (rows < minrows) rows = minrows < a.R ? minrows : a.R;
     if (rmax > 0 && rows > rmax) rows = rmax;

@@ -111,7 +111,7 @@ constexpr int TM_GUNITS = 12 * 256;  // x-gather copy units per CTA (K * units p
 
 template <int NRP, int SPS, int NC>
 __global__ void __launch_bounds__(32 * (NC + 1), 1)
-    gemv_tma_kernel(const __grid_constant__ CUtensorMap tm, GemvArgs a, int ns, int kst, int sb_bytes) {
+    gemv_tma_kernel(const __grid_constant__ CUtensorMap tm, GemvArgs a, int ns, int kst, int sb_bytes, int a2ld) {
   constexpr int sps = SPS;
   constexpr int MT = 32 / NC;                // m-tiles per consumer warp
   constexpr int TM_GMAX = TM_GUNITS / (NC * 32);  // x-gather copy units per consumer thread
@@ -129,6 +129,9 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1)
   double* xbuf = reinterpret_cast<double*>(base + (size_t)ns * sps * sb_bytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + 2 * (size_t)kp * XLD);
   uint64_t* empty = full + ns;
+  // a2ld > 0: the level-shared tail operator (leaf down: the lift L) staged here once per CTA,
+  // rows padded to a2ld (== 4 mod 16: conflict-free fragments), rows past R2 zero
+  double* a2s = reinterpret_cast<double*>(empty + ns);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const unsigned slab_tx = (unsigned)R * 128u;
@@ -201,6 +204,15 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1)
   };
 
   for (int e = tid; e < 2 * kp * XLD; e += NC * 32) xbuf[e] = 0.0;
+  if (a2ld) {
+    // static data: before the launch wait
+    const double* A2 = a.A2.get(0);
+    const int r2p = (a.R2 + 7) & ~7;
+    for (int e = tid; e < r2p * a2ld; e += NC * 32) {
+      const int r = e / a2ld, k = e - r * a2ld;
+      a2s[e] = (r < a.R2 && k < a.K2) ? __ldg(A2 + (long long)r * a.A2.ld + k) : 0.0;
+    }
+  }
   consumers_sync<NC>();
   pdl_wait();  // the pool (x) is produced by the previous step
   if (blockIdx.x < a.nitems) {
@@ -256,57 +268,46 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1)
       orows[i] = r < R ? __ldg(oi + r) : 0;
       arows[i] = (ai && r < R) ? __ldg(ai + r) : -1;
     }
-    for (int ks = 0; ks < kst; ++ks) {
-      mbar_wait(full + slot, ph);
-      const int nq = min(sps, nslab - ks * sps);
-      // the tile count is warp-uniform: dispatch to a branch-free body per count (a guarded
-      // DMMA compiles to a predicated one, which still occupies the tensor pipe)
-      switch (ntw) {
-        case 1: stage_mma<1, NT, XLD, SPS, NC, MT>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
-        case 2: stage_mma<(MT >= 2 ? 2 : 1), NT, XLD, SPS, NC, MT>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
-        case 3: stage_mma<(MT >= 3 ? 3 : 1), NT, XLD, SPS, NC, MT>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
-        case 4: stage_mma<(MT >= 4 ? 4 : 1), NT, XLD, SPS, NC, MT>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
-        default: break;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + slot);
-      if (++slot == ns) {
-        slot = 0;
-        ph ^= 1u;
-      }
-    }
-    // epilogue: y rows -> pool (+ add rows)
-#pragma unroll
-    for (int i = 0; i < MT; ++i) {
-      const int r = (warp + i * NC) * 8 + rg;
-      if (r >= R) continue;
-      const long long orow = (long long)orows[i] * nrhs;
-      const long long arow = arows[i] >= 0 ? (long long)arows[i] * nrhs : -1;
-#pragma unroll
-      for (int n = 0; n < NT; ++n)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int j = n * 8 + 2 * t + h;
-          if (j < nrhs) {
-            double v = acc[0][i][n][h] + acc[1][i][n][h];
-            if (arow >= 0) v += a.pool[arow + j];
-            a.pool[orow + j] = v;
-          }
-        }
-    }
     if (a.mode2 == 1) {
-      // tail: y2 = A2 x[K-K2:K); A2 shared by the level (lift L), read through L1
+      // tail: y2 = A2 x[K-K2:K); A2 shared by the level (lift L). It depends on x only, so it runs
+      // BEFORE the main loop, on the warps that own fewer m-tiles (the upper half), while the
+      // first slabs of the item are still in flight: no serial tail phase at the end of an item
       const double* A2 = a.A2.get(item);
       const int ld2 = a.A2.ld, K2 = a.K2, R2 = a.R2, x0 = K - K2;
       const int* o2 = a.o2idx + (long long)item * R2;
       const int* a2 = a.a2idx ? a.a2idx + (long long)item * R2 : nullptr;
-      for (int tile = warp; tile * 8 < R2; tile += NC) {
+      for (int tile = (warp + NC / 2) % NC; tile * 8 < R2; tile += NC) {
         const int ra = tile * 8 + g;
         const double* arow2 = A2 + (long long)(ra < R2 ? ra : 0) * ld2;
         double c2[NT][2];
 #pragma unroll
         for (int n = 0; n < NT; ++n) c2[n][0] = c2[n][1] = 0.0;
         int k = 0;
+        if (a2ld) {
+          // staged tail operator: two independent accumulator chains over alternating k4 steps
+          const double* as = a2s + (size_t)ra * a2ld;
+          double c3[NT][2];
+#pragma unroll
+          for (int n = 0; n < NT; ++n) c3[n][0] = c3[n][1] = 0.0;
+          for (; k + 8 <= K2; k += 8) {
+            const double a0 = as[k + t], a1 = as[k + 4 + t];
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+              dmma_nv(c2[n][0], c2[n][1], a0, xc[(x0 + k + t) * XLD + n * 8 + g]);
+              dmma_nv(c3[n][0], c3[n][1], a1, xc[(x0 + k + 4 + t) * XLD + n * 8 + g]);
+            }
+          }
+          for (; k < K2; k += 4) {
+            const double a0 = as[k + t];
+#pragma unroll
+            for (int n = 0; n < NT; ++n) dmma_nv(c2[n][0], c2[n][1], a0, xc[(x0 + k + t) * XLD + n * 8 + g]);
+          }
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            c2[n][0] += c3[n][0];
+            c2[n][1] += c3[n][1];
+          }
+        }
         for (; k + 16 <= K2; k += 16) {
           double av[4];
 #pragma unroll
@@ -342,6 +343,61 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1)
             }
         }
       }
+    }
+    for (int ks = 0; ks < kst; ++ks) {
+      mbar_wait(full + slot, ph);
+      const int nq = min(sps, nslab - ks * sps);
+      // the tile count is warp-uniform: dispatch to a branch-free body per count (a guarded
+      // DMMA compiles to a predicated one, which still occupies the tensor pipe)
+      switch (ntw) {
+        case 1: stage_mma<1, NT, XLD, SPS, NC, MT>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
+        case 2: stage_mma<(MT >= 2 ? 2 : 1), NT, XLD, SPS, NC, MT>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
+        case 3: stage_mma<(MT >= 3 ? 3 : 1), NT, XLD, SPS, NC, MT>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
+        case 4: stage_mma<(MT >= 4 ? 4 : 1), NT, XLD, SPS, NC, MT>(acc, base, slot, sb_bytes, nq, xc, (ks * sps) * 16, aoff, warp, g, t); break;
+        default: break;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + slot);
+      if (++slot == ns) {
+        slot = 0;
+        ph ^= 1u;
+      }
+    }
+    // epilogue: y rows -> pool (+ add rows)
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int r = (warp + i * NC) * 8 + rg;
+      if (r >= R) continue;
+      const long long orow = (long long)orows[i] * nrhs;
+      const long long arow = arows[i] >= 0 ? (long long)arows[i] * nrhs : -1;
+      if (wide) {
+        // even nrhs: the pair (j, j + 1) of a lane is one 16-byte access
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const int j = n * 8 + 2 * t;
+          if (j < nrhs) {
+            double2 v = make_double2(acc[0][i][n][0] + acc[1][i][n][0], acc[0][i][n][1] + acc[1][i][n][1]);
+            if (arow >= 0) {
+              const double2 w = *reinterpret_cast<const double2*>(a.pool + arow + j);
+              v.x += w.x;
+              v.y += w.y;
+            }
+            *reinterpret_cast<double2*>(a.pool + orow + j) = v;
+          }
+        }
+        continue;
+      }
+#pragma unroll
+      for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = n * 8 + 2 * t + h;
+          if (j < nrhs) {
+            double v = acc[0][i][n][h] + acc[1][i][n][h];
+            if (arow >= 0) v += a.pool[arow + j];
+            a.pool[orow + j] = v;
+          }
+        }
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     consumers_sync<NC>();  // next X landed for everyone; this X no longer read
@@ -400,20 +456,34 @@ bool launch_gemv_tma(const GemvArgs& a, cudaStream_t s) {
   const int xld = nrp + 4;
   const int nslab = (a.K + 15) / 16;
   const int sb = ((a.R * 128 + 1023) / 1024) * 1024;
-  const size_t budget = 220 * 1024;
+  const size_t budget = 226 * 1024;
+  // the level-shared tail operator (lift) staged in shared memory when a ring of >= 4 stages
+  // still fits (HPS_TMA_A2S=0: read it through L1/L2 instead)
+  static const int a2s_on = [] {
+    const char* e = getenv("HPS_TMA_A2S");
+    return e ? atoi(e) : 1;
+  }();
+  int a2ld = 0;
+  size_t a2bytes = 0;
+  if (a2s_on && a.mode2 == 1 && a.A2.stride == 0 && !a.A2.ptrs && a.K2 % 4 == 0 && a.K2 > 0) {
+    a2ld = ((a.K2 + 11) & ~15) + 4;
+    a2bytes = sizeof(double) * (size_t)((a.R2 + 7) & ~7) * a2ld;
+  }
   // one 16-column slab per stage (wider stages measured no faster on config 5)
   int sps = 1;
   int ns = 0, kst = 0;
   size_t smem = 0;
-  for (; sps >= 1; sps >>= 1) {
+  for (int pass = 0; pass < 2; ++pass) {
     kst = (nslab + sps - 1) / sps;
     const size_t xbytes = 2 * sizeof(double) * (size_t)kst * sps * 16 * xld;
     ns = 8;
-    while (ns > 2 && 1024 + (size_t)ns * sps * sb + xbytes + 16 * ns > budget) --ns;
-    smem = 1024 + (size_t)ns * sps * sb + xbytes + 16 * (size_t)ns;
-    if (smem <= budget && (ns >= 3 || sps == 1)) break;
+    while (ns > 2 && 1024 + (size_t)ns * sps * sb + xbytes + 16 * ns + a2bytes > budget) --ns;
+    smem = 1024 + (size_t)ns * sps * sb + xbytes + 16 * (size_t)ns + a2bytes;
+    if (smem <= budget && (ns >= 4 || !a2ld)) break;
+    a2ld = 0;  // not enough room for the staged tail operator and a deep enough ring
+    a2bytes = 0;
   }
-  if (sps < 1 || smem > budget) return false;
+  if (smem > budget || ns < 2) return false;
 
   CUtensorMap tm;
   const cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)a.nitems * a.R};
@@ -434,7 +504,7 @@ bool launch_gemv_tma(const GemvArgs& a, cudaStream_t s) {
     const char* e = getenv("HPS_TMA_NC");
     return (e && atoi(e) == 8) ? 8 : 16;
   }();
-  using KFn = void (*)(const CUtensorMap, GemvArgs, int, int, int);
+  using KFn = void (*)(const CUtensorMap, GemvArgs, int, int, int, int);
   const KFn k = nc == 16 ? (nrp == 16 ? gemv_tma_kernel<16, 1, 16> : gemv_tma_kernel<8, 1, 16>)
                          : (nrp == 16 ? gemv_tma_kernel<16, 1, 8> : gemv_tma_kernel<8, 1, 8>);
   static bool configured[2] = {};
@@ -452,7 +522,7 @@ bool launch_gemv_tma(const GemvArgs& a, cudaStream_t s) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k, tm, a, ns, kst, sb) == cudaSuccess;
+  return cudaLaunchKernelEx(&cfg, k, tm, a, ns, kst, sb, a2ld) == cudaSuccess;
 }
 
 // ---------------------------------------------------------------------------------------------

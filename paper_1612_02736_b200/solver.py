@@ -409,9 +409,10 @@ class FactorizedSolver:
             rm = self._leaf_rowmap = {int(n): r for r, n in enumerate(self._leaf_ids)}
         return LeafSolutions(None, None, table, rowmap=rm)
 
-    def _leaf_table(self, g, out=None):
+    def _leaf_table(self, g, out=None, rows=None):
         """(n_leaves, m) interior body-load table in leaf-row order (solver.py:241-253). With
-        `out` (an (n_leaves, m) float64 array) a mapping input is gathered straight into it."""
+        `out` (an (n_leaves, m) float64 array) a mapping input is gathered straight into it;
+        rows = (r0, r1) gathers that leaf-row range of a mapping into `out` ((r1 - r0, m))."""
         if g is None:
             g = self.spec.body_load
         nl = self._n_leaves
@@ -439,15 +440,16 @@ class FactorizedSolver:
                 return out
         # mapping {leaf id: (m,)} (reference solver.py:246-252): one gather in leaf-row order,
         # concatenated in C into the destination (no per-leaf Python work beyond the lookups)
-        vals = [g[nid] for nid in self._leaf_ids]
-        dst = out if out is not None else np.empty((nl, m))
+        ids = self._leaf_ids if rows is None else self._leaf_ids[rows[0]:rows[1]]
+        vals = [g[nid] for nid in ids]
+        dst = out if out is not None else np.empty((len(ids), m))
         try:
             if set(map(len, vals)) == {m}:
                 np.concatenate(vals, out=dst.reshape(-1))
                 return dst
         except (TypeError, ValueError):
             pass
-        for nid, v in zip(self._leaf_ids, vals):
+        for nid, v in zip(ids, vals):
             shp = np.shape(v)
             if shp != (m,):
                 raise ValueError(f"leaf {nid} load has shape {shp}, expected ({m},)")
