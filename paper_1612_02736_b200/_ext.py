@@ -125,3 +125,27 @@ def mat(tensor_or_ptr, stride: int, ld: int, off: int = 0, ptrs=None) -> MatBatc
 
 def ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
+
+
+_host = False
+
+
+def host_module():
+    """The optional CPython helper `_hps_host` (threaded gather of body-load mappings), or None."""
+    global _host
+    if _host is False:
+        _host = None
+        try:
+            path = build_ext.build_host()
+            if path:
+                import importlib.machinery
+                import importlib.util
+                loader = importlib.machinery.ExtensionFileLoader("_hps_host", path)
+                spec = importlib.util.spec_from_loader("_hps_host", loader)
+                mod = importlib.util.module_from_spec(spec)
+                loader.exec_module(mod)
+                _host = mod
+        except Exception:
+            _host = None
+    return _host
+

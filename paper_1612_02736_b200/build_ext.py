@@ -26,11 +26,41 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found; the HPS extension needs the CUDA 12.9 toolkit")
 
 
+HOST_LIB = os.path.join(PKG, "_hps_host.so")
+HOST_SRC = os.path.join(CSRC, "host_gather.cpp")
+
+
+def build_host(force: bool = False) -> str | None:
+    """Compile the CPython helper module `_hps_host` (host-side gather of body-load mappings; not
+    on the device path). Returns its path, or None when no host compiler / headers are available
+    (solver.py then uses its numpy path)."""
+    if not force and os.path.exists(HOST_LIB) and os.path.getmtime(HOST_LIB) >= os.path.getmtime(HOST_SRC):
+        return HOST_LIB
+    import sysconfig
+    try:
+        import numpy
+        cxx = shutil.which("g++") or shutil.which("c++")
+        if not cxx:
+            return None
+        cmd = [cxx, "-O3", "-std=c++17", "-shared", "-fPIC", "-pthread", "-I", sysconfig.get_paths()["include"],
+               "-I", numpy.get_include(), HOST_SRC, "-o", HOST_LIB + ".tmp"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            return None
+        os.replace(HOST_LIB + ".tmp", HOST_LIB)
+        return HOST_LIB
+    except Exception as exc:  # host helper is optional
+        sys.stderr.write(f"_hps_host not built: {exc}\n")
+        return None
+
+
 def up_to_date() -> bool:
     if not os.path.exists(LIB):
         return False
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "hps_b200.h")]
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if not f.endswith(".cpp")]
+    deps.append(os.path.join(ROOT, "include", "hps_b200.h"))
     return all(os.path.getmtime(d) <= t for d in deps if os.path.exists(d))
 
 
@@ -45,6 +75,7 @@ def _headers():
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile each source to an object (in parallel; a source is recompiled when it or any
     header is newer than its object), then link the shared library."""
+    build_host(force)
     if not force and up_to_date():
         return LIB
     from concurrent.futures import ThreadPoolExecutor

@@ -897,10 +897,36 @@ bool launch_gemv_stream(const GemvArgs& a, cudaStream_t s) {
   if (!enc) return false;
 
   StreamCfg c{};
-  // row blocks: the whole item when it has <= 256 rows, else equal blocks rounded up to m-tiles
-  const int nb = (a.R + 255) / 256;
-  c.RB = nb == 1 ? a.R : (((a.R + nb - 1) / nb) + 7) & ~7;
-  c.nrb = (a.R + c.RB - 1) / c.RB;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // row blocks: equal blocks of <= 256 rows rounded up to m-tiles. Units (item x row block) are
+  // dealt round-robin to one persistent CTA per SM and a 256-row unit is ~10 us of one SM's HBM
+  // share, so the block count is chosen for whole waves: the fewest blocks whose unit count fills
+  // >= 95 % of its last wave, else the best fill among blocks of >= 64 rows (config 5, 16 RHS:
+  // 300-336 units were 2.03-2.27 waves = 68-76 % fill)
+  {
+    static const int balance = [] {
+      const char* e = getenv("HPS_STREAM_BALANCE");
+      return e ? atoi(e) : 1;
+    }();
+    const int nb0 = (a.R + 255) / 256;
+    int best_nb = nb0;
+    double best_eff = 0.0;
+    const int nb_max = balance ? std::max(nb0, (a.R + 63) / 64) : nb0;
+    for (int nb = nb0; nb <= nb_max; ++nb) {
+      const int rb = nb == 1 ? a.R : (((a.R + nb - 1) / nb) + 7) & ~7;
+      const long long u = (long long)a.nitems * ((a.R + rb - 1) / rb);
+      const double eff = (double)u / ((double)sms * (double)((u + sms - 1) / sms));
+      if (eff > best_eff + 0.02) {
+        best_eff = eff;
+        best_nb = nb;
+      }
+      if (eff >= 0.95) break;
+    }
+    c.RB = best_nb == 1 ? a.R : (((a.R + best_nb - 1) / best_nb) + 7) & ~7;
+    c.nrb = (a.R + c.RB - 1) / c.RB;
+  }
   c.KX = 128;
   c.sb_bytes = ((c.RB * 128 + 1023) / 1024) * 1024;
   const int nrp = a.nrhs <= 8 ? 8 : 16;
@@ -924,9 +950,6 @@ bool launch_gemv_stream(const GemvArgs& a, cudaStream_t s) {
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long units = (long long)a.nitems * c.nrb;
   const int grid = (int)(units < sms ? units : sms);
   using KFn = void (*)(const CUtensorMap, GemvArgs, StreamCfg);

@@ -41,6 +41,12 @@ _SPLIT_CTAS = int(os.environ.get("HPS_SPLIT_CTAS", "600"))  # split-K when a ste
 BUILD_COUNT = 0
 
 
+# copy threads of the host-side load gather (_hps_host): more threads make the gather itself faster
+# (0.42 -> 0.20 ms for config 2 with 4) but the whole host-API solve slower (1.46 -> 1.77 ms: the
+# thread starts compete with the launch / copy-polling path), so one thread is the default
+_HOST_THREADS = max(1, min(8, int(os.environ.get("HPS_HOST_THREADS", "1"))))
+
+
 class LeafSingularError(RuntimeError):
     """Interior collocation block is (numerically) singular on some leaf."""
 
@@ -441,8 +447,17 @@ class FactorizedSolver:
         # mapping {leaf id: (m,)} (reference solver.py:246-252): one gather in leaf-row order,
         # concatenated in C into the destination (no per-leaf Python work beyond the lookups)
         ids = self._leaf_ids if rows is None else self._leaf_ids[rows[0]:rows[1]]
-        vals = [g[nid] for nid in ids]
         dst = out if out is not None else np.empty((len(ids), m))
+        host = _ext.host_module()
+        if host is not None and rows is None and dst.dtype == np.float64 and dst.flags.c_contiguous:
+            # threaded C gather (lookups and shape checks under the GIL, row copies without it);
+            # anything but contiguous float64 (m,) rows falls through to the generic path below
+            idl = getattr(self, "_leaf_id_list", None)
+            if idl is None:
+                idl = self._leaf_id_list = [int(n) for n in self._leaf_ids]
+            if host.gather_rows(g, idl, dst, _HOST_THREADS) < 0:
+                return dst
+        vals = [g[nid] for nid in ids]
         try:
             if set(map(len, vals)) == {m}:
                 np.concatenate(vals, out=dst.reshape(-1))
@@ -505,6 +520,23 @@ class FactorizedSolver:
         stage = prog.get("g_stage")
         if stage is None:
             stage = prog["g_stage"] = torch.empty(nl * m, dtype=torch.float64, pin_memory=True)
+        host = _ext.host_module() if isinstance(g, Mapping) and nl >= 2048 else None
+        if host is not None and not isinstance(g, LeafSolutions):
+            # large mapping: gathered into the page-locked stage in leaf ranges by the C helper,
+            # each range's host->device copy running while the next range is gathered
+            idl = getattr(self, "_leaf_id_list", None)
+            if idl is None:
+                idl = self._leaf_id_list = [int(n) for n in self._leaf_ids]
+            stage_np = stage.numpy().reshape(nl, m)
+            nch, done = 4, 0
+            for c_ in range(nch):
+                r0, r1 = nl * c_ // nch, nl * (c_ + 1) // nch
+                if host.gather_rows(g, idl[r0:r1], stage_np[r0:r1], _HOST_THREADS) >= 0:
+                    break  # a value the fast path does not take: generic path below
+                g_rows[r0 * m:r1 * m].copy_(stage[r0 * m:r1 * m], non_blocking=True)
+                done = r1
+            if done == nl:
+                return g
         if isinstance(g, Mapping):
             self._leaf_table(g, out=stage.numpy().reshape(nl, m))
             tab = g
