@@ -15,7 +15,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "_hps_b200.so")
-SOURCES = ("hps_abi.cu", "gemm_dmma.cu", "gj.cu", "gj_fused.cu", "gj_cluster.cu", "gj_pair.cu", "leaf_merge.cu", "sweep.cu", "sweep_tma.cu", "leaf_apply.cu")
+SOURCES = ("hps_abi.cu", "gemm_dmma.cu", "gj.cu", "gj_fused.cu", "gj_cluster.cu", "gj_pair.cu", "gj_la.cu", "leaf_merge.cu", "sweep.cu", "sweep_tma.cu", "leaf_apply.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -456,6 +456,7 @@ int gj_invert(int batch, int n, int ncols, MatB M, int* piv, double* wbuf, doubl
       const char* e = getenv("HPS_GJ_FUSED_PER_SM");
       per_sm = e ? atoi(e) : 2;
     }
+    if (gj_la_ok(n, ncols) && batch >= sms) return launch_gj_la(f, s);
     if (gj_pair_ok(n, ncols)) return launch_gj_pair(f, s);
     const int grid = batch < per_sm * sms ? batch : per_sm * sms;
     return launch_gj_fused(f, grid, s);

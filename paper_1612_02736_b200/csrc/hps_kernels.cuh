@@ -52,6 +52,9 @@ int launch_gj_fused(const FusedArgs& a, int grid, cudaStream_t s);
 // small matrices resident in a 2-CTA cluster's shared memory (gj_pair.cu; full mode)
 bool gj_pair_ok(int n, int ncols);
 int launch_gj_pair(const FusedArgs& a, cudaStream_t s);
+// warp-specialised look-ahead kernel for the p = 16 leaf blocks (gj_la.cu; full mode)
+bool gj_la_ok(int n, int ncols);
+int launch_gj_la(const FusedArgs& a, cudaStream_t s);
 
 // Leaf-stage assembly: interior rows of the collocation matrix for each leaf.
 struct LeafAsmArgs {

@@ -139,3 +139,18 @@ def test_gj_pair_kernel_opt_in():
                         "-k", "gj_inverse or gj_pivot or gj_permuted or gj_flags"],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_gj_lookahead_kernel_opt_in():
+    """The warp-specialised look-ahead Gauss-Jordan kernel (csrc/gj_la.cu, opt-in with HPS_GJ_LA=1,
+    read once per process; taken for 56 < n <= 224 with >= 148 matrices) passes the same inverse /
+    permuted-output checks, several matrices per persistent CTA included."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, HPS_GJ_LA="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", __file__,
+                        "-k", "(gj_inverse and (196 or 130)) or gj_permuted"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
