@@ -462,7 +462,9 @@ __global__ void __launch_bounds__(LA_THREADS, 1) gj_la_kernel(FusedArgs a) {
           la_stage_w(Mi, ld, C, kbc, Wu, ldw, cw, ldw, cmap, ut, LA_UT);
           bar_u();
           LA_T(10);  // U: stage W
+#ifndef LA_SKIP_U  // (timing experiment: panel group alone; results are wrong)
           la_update_tiles(Mi, ld, n, k0, kbc, Pk, ldp, Wu, ldw, cw, cmap, uw, LA_UW, lane);
+#endif
           bar_u();
           LA_T(11);  // U: tiles
         }
