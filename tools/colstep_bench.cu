@@ -19,7 +19,8 @@ enum : unsigned {
   F_UNIFORM = 256, // publication behind warp-uniform branches
   F_PRESCALE = 512, // winner publishes the scaled row; elimination is LDS + DFMA only
   F_INTKEY = 1024,  // arg-max on the bit pattern of |v| (integer compares), indices kept as ints
-  F_VEC = 2048      // 16-byte shared stores / loads for the published rows
+  F_VEC = 2048,     // 16-byte shared stores / loads for the published rows
+  F_UELIM = 4096    // elimination: warps without a special row run a bare update
 };
 
 template <unsigned F, int NT>
@@ -187,7 +188,17 @@ __global__ void __launch_bounds__(NT, 1) colstep(double* out, int* piv, int ncol
         }
         double inv = 0.5;
         if ((F & F_DIVIDE) && !(F & F_PRESCALE)) inv = 1.0 / pvr[q];
-        if (F & F_ELIM) {
+        if ((F & F_ELIM) && (F & F_UELIM) && (cj >> 5) != warp && ((pr >> 5) != warp || pr == cj)) {
+          // no special row in this warp: bare update
+          const double f = row[q];
+          if (F & F_PRESCALE) {
+#pragma unroll
+            for (int t = 0; t < KB; ++t) row[t] = ((t == q) ? 0.0 : row[t]) - f * pvr[t];
+          } else {
+#pragma unroll
+            for (int t = 0; t < KB; ++t) row[t] = ((t == q) ? 0.0 : row[t]) - f * ((t == q) ? inv : pvr[t] * inv);
+          }
+        } else if (F & F_ELIM) {
           if (i == pr && pr != cj) {
 #pragma unroll
             for (int t = 0; t < KB; ++t) row[t] = disp[t];
@@ -282,6 +293,9 @@ int main() {
   run<ALL | F_PRESCALE | F_VEC, 256>("+ prescale + vec", out, piv, cyc);
   run<ALL | F_PRESCALE | F_VEC | F_INTKEY, 256>("+ prescale + vec + intkey", out, piv, cyc);
   run<ALL | F_PRESCALE | F_VEC | F_INTKEY | F_UNIFORM, 256>("+ prescale + vec + intkey + unif", out, piv, cyc);
+  run<ALL | F_UELIM, 256>("+ uniform elimination", out, piv, cyc);
+  run<ALL | F_UELIM | F_UNIFORM, 256>("+ uniform elim + publish", out, piv, cyc);
+  run<ALL | F_UELIM | F_UNIFORM | F_PRESCALE | F_INTKEY, 256>("+ uelim + upub + prescale + intkey", out, piv, cyc);
   run<F_BARRIER, 256>("barrier only", out, piv, cyc);
   run<F_BARRIER | F_ELIM | F_DIVIDE, 256>("barrier + divide + eliminate", out, piv, cyc);
   run<F_REDUCE1 | F_BARRIER | F_REDUCE2, 256>("reduces + barrier", out, piv, cyc);
