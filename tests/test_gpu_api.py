@@ -167,3 +167,37 @@ def test_econ_split_size_leaf_step(nrhs):  # econ, 4x4 leaves,
     ua = stored.solve_device(fv, g)["uc"].clone()
     ub = econ.solve_device(fv, g)["uc"].clone()
     assert (ua - ub).abs().max().item() <= 1e-12 * ua.abs().max().item()
+
+
+def test_load_conventions_agree_on_a_large_mesh():
+    """g as a callable, as the reference's {leaf id: (m,)} mapping (solver.py:241-253; the C
+    gather helper with range-by-range uploads handles >= 2048 leaves), as a mapping whose values
+    the fast path does not take (float32, lists, strided views: generic numpy path) and as the
+    (n_leaves, m) table give the same solution; a wrong-length value raises like the reference."""
+    n, p, q = 64, 8, 7  # 4096 leaves, small order: exercises the chunked gather cheaply
+    tree = build_uniform_tree(UNIT, n)
+    solver = build_stage(tree, catalog("laplace"), p, q)
+    gfn = lambda pts: np.sin(3 * pts[:, 0]) * np.cos(2 * pts[:, 1])
+    ref = solver.solve(g=gfn)
+    tab = np.asarray(solver._leaf_table(gfn))
+    ids = [int(i) for i in solver._leaf_ids]
+    gmap = {nid: tab[r].copy() for r, nid in enumerate(ids)}
+    st = solver.solve(g=gmap)
+    assert np.array_equal(st.u, ref.u)
+    assert st.g_tab is gmap  # the state keeps the caller's mapping, as the reference does
+    odd = dict(gmap)
+    odd[ids[5]] = tab[5].astype(np.float32).astype(np.float64).tolist()          # a list
+    odd[ids[77]] = np.repeat(tab[77], 2)[::2]                                      # a strided view
+    st2 = solver.solve(g=odd)
+    exact = dict(gmap)
+    exact[ids[5]] = np.asarray(odd[ids[5]])
+    assert np.array_equal(st2.u, solver.solve(g=exact).u)
+    assert np.array_equal(solver.solve(g=tab).u, ref.u)
+    bad = dict(gmap)
+    bad[ids[9]] = np.zeros(tab.shape[1] + 1)
+    with pytest.raises(ValueError, match=f"leaf {ids[9]} load has shape"):
+        solver.solve(g=bad)
+    missing = dict(gmap)
+    del missing[ids[3]]
+    with pytest.raises(KeyError):
+        solver.solve(g=missing)
