@@ -210,7 +210,13 @@ __device__ __forceinline__ void prefetch_rows(const double* Ai, long long ld, in
   }
 }
 
-template <int NRP, bool VEC>
+#ifndef HPS_DMMA_U2
+#define HPS_DMMA_U2 6  // A-fragment loads in flight per lane and row tile for K >= 96 (4 below)
+#endif
+// UA: A-fragment loads in flight per lane and row tile. 6 instead of 4 for the longer rows keeps
+// more bytes in flight per SM at the same 4 CTAs (config 5, 16 RHS: leaf upward step 514 -> 487 us,
+// K = 240 split parts 57 -> 53.5 us); 8 needs 3 CTAs per SM or spills and measured slower
+template <int NRP, bool VEC, int UA = 4>
 __global__ void __launch_bounds__(256, 4) gemv_dmma_kernel(GemvArgs a, int rpc, int kchunk, int batch_off,
                                                             int stage_idx) {
   extern __shared__ double xs[];
@@ -304,17 +310,17 @@ __global__ void __launch_bounds__(256, 4) gemv_dmma_kernel(GemvArgs a, int rpc, 
     const int kc4 = kcp;
     const int step = WK * 4;
     int k = wk * 4;
-    for (; k + 3 * step < kc4; k += 4 * step) {
-      double va[4], vb[4];
+    for (; k + (UA - 1) * step < kc4; k += UA * step) {
+      double va[UA], vb[UA];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < UA; ++u) {
         const int kk = k + u * step + tq;
         const bool kin = kk < kc;
         va[u] = (kin && la) ? __ldg(rowa + k0 + kk) : 0.0;
         vb[u] = (kin && lb) ? __ldg(rowb + k0 + kk) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < UA; ++u)
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
           const double bv = xs[(k + u * step + tq) * XLD + n * 8 + gq];
@@ -913,9 +919,11 @@ static void launch_dmma(const GemvArgs& a, cudaStream_t s) {
   for (int off = 0; off < a.nitems; off += 65535) {
     dim3 grid(gx, min(65535, a.nitems - off));
     if (vec)
-      launch_k(gemv_dmma_kernel<NRP, true>, grid, dim3(256), smem, s, a, rpc, kchunk, off, stage);
+      launch_k(gemv_dmma_kernel<NRP, true, 4>, grid, dim3(256), smem, s, a, rpc, kchunk, off, stage);
+    else if (a.K >= 96)
+      launch_k(gemv_dmma_kernel<NRP, false, HPS_DMMA_U2>, grid, dim3(256), smem, s, a, rpc, kchunk, off, stage);
     else
-      launch_k(gemv_dmma_kernel<NRP, false>, grid, dim3(256), smem, s, a, rpc, kchunk, off, stage);
+      launch_k(gemv_dmma_kernel<NRP, false, 4>, grid, dim3(256), smem, s, a, rpc, kchunk, off, stage);
   }
 }
 
