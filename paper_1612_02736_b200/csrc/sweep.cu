@@ -370,12 +370,31 @@ __global__ void __launch_bounds__(256, 4) gemv_dmma_kernel(GemvArgs a, int rpc, 
   const int* ai = a.aidx ? a.aidx + (long long)item * a.ostride : nullptr;
   const int* oi = a.oidx + (long long)item * a.ostride;
   double* pw = a.pool;
+  // even nrhs on a 16-byte aligned pool: the pair (j, j + 1) of a lane is one 16-byte access (the
+  // deep levels move more vector bytes than operator bytes)
+  const bool wide = (nrhs & 1) == 0 && (reinterpret_cast<uintptr_t>(pw) & 15) == 0;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int r = i ? rb : ra;
     if (r >= R) continue;
     const long long orow = (long long)oi[r] * nrhs;
     const long long arow = ai ? (long long)ai[r] * nrhs : -1;
+    if (wide) {
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        const int j = n * 8 + tq * 2;
+        if (j < nrhs) {
+          double2 v = make_double2(acc[i][n][0], acc[i][n][1]);
+          if (arow >= 0) {
+            const double2 w = *reinterpret_cast<const double2*>(pool + arow + j);
+            v.x += w.x;
+            v.y += w.y;
+          }
+          *reinterpret_cast<double2*>(pw + orow + j) = v;
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int n = 0; n < NT; ++n)
 #pragma unroll
