@@ -120,6 +120,9 @@ __device__ __forceinline__ const double* gemv_a(const GemvArgs& a, int i) {
   return a.kparts > 1 ? a.A.get(i / a.kparts) + (long long)(i % a.kparts) * a.K : a.A.get(i);
 }
 int launch_gemv_gather(const GemvArgs& a, cudaStream_t s);
+// programmatic dependent launch for a step with this many right-hand sides on a persistent (one
+// CTA per SM, TMA-fed) or many-CTA kernel (HPS_PDL; sweep.cu)
+bool sweep_pdl_for(int nrhs, bool persistent);
 // TMA-fed multi-RHS path for large leaf levels (sweep_tma.cu); false = not applicable
 bool launch_gemv_tma(const GemvArgs& a, cudaStream_t s);
 // TMA-streamed multi-RHS path for large operator items (top levels, split-K parts; sweep_tma.cu)

@@ -521,7 +521,7 @@ bool launch_gemv_tma(const GemvArgs& a, cudaStream_t s) {
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = sweep_pdl_for(a.nrhs, true) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, tm, a, ns, kst, sb, a2ld) == cudaSuccess;
 }
 
@@ -968,7 +968,7 @@ bool launch_gemv_stream(const GemvArgs& a, cudaStream_t s) {
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = sweep_pdl_for(a.nrhs, true) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, tm, a, c) == cudaSuccess;
 }
 
